@@ -1,0 +1,211 @@
+/*
+ * spmv.h -- C ABI of the B200-native tiled-composite SpMV library (libtcspmv.so).
+ *
+ * Method: Yang, Parthasarathy & Sadayappan, "Fast Sparse Matrix-Vector Multiplication on GPUs:
+ * Implications for Graph Mining", PVLDB 4(4), 2011 (cited as PAPER.md Lnn = line of the text).
+ *
+ * The library computes y = A x for an n_rows x n_cols sparse matrix A in CSR (PAPER.md L291,
+ * App. B problem statement) through the paper's TILE-COMPOSITE representation:
+ *   - columns reordered by decreasing length (Solution 2, L66),
+ *   - the dense leading columns cut into fixed-width tiles whose x segment stays on chip
+ *     (Solution 1, L56-L60; Alg. 1), the rest one composite remainder tile (L90-L92),
+ *   - inside each tile, rows ranked by length and packed into ~WL-entry workloads, each a w x h
+ *     rectangle run by one warp: row major / CSR-vector when w >= h, column major / ELL otherwise
+ *     (Solution 3, L88, L94),
+ * and the power iterations PageRank (Eq. 6), HITS (Eq. 8) and Random Walk with
+ * Restart (Eq. 9) on top of it, on one B200 or row-partitioned over several (Sec. 3.2).
+ *
+ * Conventions for every function:
+ *   - returns spmv_status; SPMV_OK = 0.  Nothing throws or aborts across this boundary; the
+ *     message of the last non-OK status of the calling thread is spmv_last_error().
+ *   - host input arrays are borrowed for the duration of the call and copied; the caller keeps
+ *     ownership.  "_dev" pointers are device pointers owned by the caller (e.g. torch tensors).
+ *   - streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - indices: row_ptr int64 (nnz may exceed 2^31), column ids int32, n_rows < 2^29.
+ *   - there is no CPU fallback: without a CUDA device every device entry point returns
+ *     SPMV_ECUDA.
+ */
+#ifndef TCSPMV_H
+#define TCSPMV_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPMV_OK = 0,
+    SPMV_EINVAL = 1,      /* null pointer, negative size, row_ptr not monotone, column out of range,
+                             bad option value */
+    SPMV_EDIM = 2,        /* inconsistent dimensions */
+    SPMV_ENOTSQUARE = 3,  /* graph algorithm given a non-square matrix */
+    SPMV_ERANGE = 4,      /* query >= n, P > rows, n_rows >= 2^29, too many tiles */
+    SPMV_EROWSPLIT = 5,   /* split_long_rows = 0 and a workload size is below the tile's longest row */
+    SPMV_ETABLE = 6,      /* performance table missing or malformed */
+    SPMV_ENOMEM = 7,      /* host or device allocation failed */
+    SPMV_ECUDA = 8,       /* CUDA runtime error, or no device */
+    SPMV_ENCCL = 9,       /* NCCL error */
+    SPMV_ENOCONV = 10     /* max_iter reached before tol; outputs are still written */
+} spmv_status;
+
+typedef struct spmv_plan_s* spmv_plan;
+typedef struct spmv_comm_s* spmv_comm;
+typedef struct spmv_solver_s* spmv_solver;
+
+/* Options of the format builder (Sec. 3.1) and of the auto-tuner (Sec. 3.3).
+ * spmv_options_default() fills: tile_width 0 (auto), num_tiles -1 (auto), workload_size -1
+ * (auto), workload_sizes NULL, align_rm 8, split_long_rows 1, camping_pad 0, pattern 0,
+ * ell_h 32, stage_x 1, perf_table_path NULL. */
+typedef struct {
+    int32_t tile_width;      /* columns per dense tile (paper: 64K, L60); 0 = chosen by the tuner */
+    int32_t num_tiles;       /* dense tiles before the remainder; -1 = auto (Alg. 1 + B200 model);
+                                0 = single composite tile (the whole matrix is the remainder) */
+    int32_t workload_size;   /* WL for every tile; -1 = auto per tile (Alg. 2) */
+    const int32_t* workload_sizes; /* optional, num_tiles + 1 explicit WLs (last = remainder) */
+    int32_t align_rm;        /* row-major width alignment in slots (paper: warp size 32, L88;
+                                B200 default 8 = one 32-byte sector); multiple of 4 on device */
+    int32_t split_long_rows; /* 1: rows longer than WL become one-row chunks combined in chunk
+                                order (B200; reading R21).  0: paper lower bound WL >= longest row */
+    int32_t camping_pad;     /* 1: +64 slots after workloads of 512k slots (L96); default 0 */
+    int32_t pattern;         /* 1: values implicitly 1.0 (val may be NULL) */
+    int32_t ell_h;           /* column-major slab height (warp size); must be 32 to execute */
+    int32_t stage_x;         /* 1: dense tiles stage their x segment in shared memory */
+    const char* perf_table_path; /* JSON offline table (Sec. 3.3); NULL = built-in B200 table */
+} spmv_options;
+
+void spmv_options_default(spmv_options* opt);
+
+/* Summary of a built plan. */
+typedef struct {
+    int64_t n_rows, n_cols, nnz;
+    int32_t num_tiles;          /* dense tiles (the remainder tile is extra) */
+    int32_t tile_width;
+    int64_t n_workloads, n_slots, n_row_entries, n_split, n_chunks;
+    int64_t device_bytes;       /* device memory held by the plan */
+    double predicted_us;        /* performance-model estimate of one spmv_execute (Eq. 2) */
+    double build_ms;            /* host build time */
+    int32_t wl[64];             /* per tile WL (tile i < num_tiles; [num_tiles] = remainder) */
+    int64_t tile_nnz[64];
+    int64_t tile_rows[64];      /* rows touched per tile */
+    int64_t tile_col_lo[64], tile_col_hi[64];
+    int32_t tile_staged[64];
+    double tile_predicted_us[64];
+    int32_t composite_threshold[64]; /* first row length stored column major in each tile */
+} spmv_plan_stats_t;
+
+/* Host view of the layout arrays (Format v1), valid while the plan lives, when the
+ * plan keeps its host copy (host-only plans always do).  All pointers are plan-owned. */
+typedef struct {
+    int64_t n_cols, n_workloads, n_row_entries, n_slots, n_split, n_tiles_total;
+    const int32_t* perm;        /* [n_cols] relabelled position -> original column */
+    const int64_t* tiles;       /* [n_tiles_total][4] col_lo, col_hi, wl_begin, wl_end */
+    const int64_t* desc_off;    /* per workload: first slot */
+    const int32_t* desc_row_base, *desc_w, *desc_h, *desc_split_id, *desc_chunk;
+    const uint8_t* desc_kind, *desc_kvec;
+    const uint32_t* row_id;     /* row | 1<<29 (accumulate) | 1<<30 (final); 0xFFFFFFFF = pad */
+    const int32_t* slot_col;    /* tile-relative column; sentinel = tile width */
+    const float* slot_val;      /* NULL for pattern plans */
+    const int32_t* split;       /* [n_split][3] row entry, n_chunks, partial_base */
+} spmv_layout_view;
+
+/* Build the tiled-composite plan of A (host CSR, copied) and upload it to `device`.
+ * device = -1 builds a host-only plan (layout inspection / export; cannot execute).
+ * val may be NULL when opt->pattern = 1.  Errors: EINVAL, EDIM, ERANGE, EROWSPLIT, ENOMEM, ECUDA. */
+spmv_status spmv_plan_create(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                             const int32_t* col_idx, const float* val, const spmv_options* opt,
+                             int device, spmv_plan* out);
+void spmv_plan_destroy(spmv_plan plan);
+
+/* y = A x.  x_dev: n_cols floats in the caller's column order; y_dev: n_rows floats in the
+ * caller's row order.  Asynchronous on `stream`.  Deterministic: bitwise identical across runs. */
+spmv_status spmv_execute(spmv_plan plan, const float* x_dev, float* y_dev, void* stream);
+
+/* Same product with x already in relabelled column order (xp_dev[k] = x[perm[k]]), as the
+ * power iterations keep it; skips the x permutation kernel. */
+spmv_status spmv_execute_permuted(spmv_plan plan, const float* xp_dev, float* y_dev, void* stream);
+
+/* spmv_execute with a CUDA event between launches; synchronises and writes the device time of
+ * every launch (x permutation first, then each tile) to launch_ms[0 .. spmv_plan_launches()).
+ * For measurement (bench.py's roofline of the dominant kernel). */
+spmv_status spmv_execute_timed(spmv_plan plan, const float* x_dev, float* y_dev, void* stream,
+                               float* launch_ms, int32_t max_launches);
+
+/* Host -> device -> host convenience: copies x (host), executes, copies y back, synchronises. */
+spmv_status spmv_execute_host(spmv_plan plan, const float* x_host, float* y_host, void* stream);
+
+spmv_status spmv_plan_stats(spmv_plan plan, spmv_plan_stats_t* out);
+spmv_status spmv_plan_layout(spmv_plan plan, spmv_layout_view* out);
+/* Decode the layout back to COO (original row / column ids), padding dropped; arrays of nnz. */
+spmv_status spmv_plan_to_coo(spmv_plan plan, int32_t* rows, int32_t* cols, float* vals);
+/* Number of kernel launches one spmv_execute issues (x permutation included). */
+int32_t spmv_plan_launches(spmv_plan plan);
+
+/* ---------------------------------------------------------------- power iterations (App. F) */
+enum { SPMV_ALGO_PAGERANK = 0, SPMV_ALGO_HITS = 1, SPMV_ALGO_RWR = 2 };
+
+typedef struct {
+    double c;              /* PageRank damping (0.85, L430) / RWR c (0.9, L456); unused by HITS */
+    double tol;            /* L1 stopping threshold on the change (reading R2); default 1e-6 */
+    int32_t max_iter;      /* default 1000 */
+    int32_t hits_norm;     /* 2 = unit L2 halves (default), 1 = halves sum to 1 (paper, L440) */
+    int32_t fixed_iters;   /* > 0: run exactly this many iterations (parity at equal k) */
+} spmv_iter_opts;
+void spmv_iter_opts_default(spmv_iter_opts* o, int algo);
+
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    double residual;       /* last L1 change */
+    double ms_total;       /* device time of the iteration loop (CUDA events) */
+    double us_per_iter;
+    double predicted_us_per_iter;
+} spmv_iter_result;
+
+/* Graph input for all three: adjacency A of G = (V,E), CSR with row u listing the targets v of
+ * u -> v (A(u,v) = 1, L414); duplicates collapse, self loops are kept.
+ * A solver builds its plan once (preprocessing amortised over iterations, L98) and can run many
+ * times; `comm` = NULL runs on one GPU, else the row-partitioned multi-GPU path (Sec. 3.2). */
+spmv_status spmv_solver_create(int algo, int64_t n, int64_t m, const int64_t* row_ptr,
+                               const int32_t* col, const spmv_iter_opts* it,
+                               const spmv_options* opt, spmv_comm comm, int device,
+                               spmv_solver* out);
+/* Run the power iteration from the initial vector (RWR: query node `query`).  Synchronises. */
+spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res);
+/* Copy the result to host, in the caller's vertex order: PageRank p [n], RWR r [n],
+ * HITS authority a [n] in out0 and hub h [n] in out1. */
+spmv_status spmv_solver_result(spmv_solver s, float* out0, float* out1);
+spmv_status spmv_solver_plan_stats(spmv_solver s, spmv_plan_stats_t* out);
+int32_t spmv_solver_launches_per_iter(spmv_solver s);
+void spmv_solver_destroy(spmv_solver s);
+
+/* One-shot wrappers: create, run, copy result, destroy. */
+spmv_status pagerank(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* col,
+                     const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,
+                     int device, float* p_out, spmv_iter_result* res);
+spmv_status hits(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* col,
+                 const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,
+                 int device, float* auth_out, float* hub_out, spmv_iter_result* res);
+spmv_status rwr(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* col, int64_t query,
+                const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,
+                int device, float* r_out, spmv_iter_result* res);
+
+/* ---------------------------------------------------------------- multi-GPU (Sec. 3.2) */
+/* Bitonic (snake) partition of rows by length over P ranks (L108, reading R25):
+ * owner_out[i] in [0,P).  Row counts differ by at most 1.  Errors: EINVAL, ERANGE (P > rows). */
+spmv_status bitonic_partition(int64_t n_rows, const int64_t* row_len, int32_t P, int32_t* owner_out);
+
+/* Communicator over NCCL (loaded at run time).  nccl_unique_id: the 128-byte ncclUniqueId,
+ * created by rank 0 with spmv_comm_unique_id() and broadcast by the caller (e.g. over a torch
+ * process group).  world = 1 is valid (no NCCL calls). */
+spmv_status spmv_comm_unique_id(void* id_out_128_bytes);
+spmv_status spmv_comm_create(int rank, int world, const void* nccl_unique_id, int device,
+                             spmv_comm* out);
+void spmv_comm_destroy(spmv_comm comm);
+
+const char* spmv_last_error(void);
+const char* spmv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCSPMV_H */

@@ -1,0 +1,361 @@
+// capi.cu -- C ABI: plan creation, upload, spmv_execute (include/spmv.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "launch.cuh"
+#include "tune.h"
+
+namespace tc {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+spmv_status cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return SPMV_OK;
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SPMV_ENOMEM : SPMV_ECUDA;
+}
+
+// xp[k] = x[perm[k]] (step a7): relabel x for the tiled product
+__global__ void permute_x_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                                 float* __restrict__ xp, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < n; i += stride) xp[i] = __ldg(x + __ldcs(perm + i));
+}
+
+template <class T>
+static cudaError_t upload(T** dst, const std::vector<T>& src, int64_t& bytes) {
+    size_t nb = std::max<size_t>(src.size(), 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(dst, nb);
+    if (e) return e;
+    bytes += (int64_t)nb;
+    if (!src.empty()) e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+template <class T>
+static cudaError_t download(std::vector<T>& dst, const T* src, int64_t n) {
+    dst.resize(n);
+    if (n == 0) return cudaSuccess;
+    return cudaMemcpy(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost);
+}
+
+static void free_device(spmv_plan_s* p) {
+    if (p->device < 0) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    cudaFree(p->d_desc); cudaFree(p->d_row_id); cudaFree(p->d_col); cudaFree(p->d_val);
+    cudaFree(p->d_perm); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
+    cudaFree(p->d_counters);
+    cudaSetDevice(cur);
+}
+
+// build the plan (host) and upload it; shared by spmv_plan_create and the solvers
+spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col, const float* val, const spmv_options* opt_in,
+                        int device, spmv_plan_s** out) {
+    auto t0 = std::chrono::steady_clock::now();
+    spmv_options opt;
+    if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
+    if (device >= 0 && (opt.ell_h != 32 || opt.align_rm % 4 != 0)) {
+        set_error("device plans need ell_h = 32 and align_rm % 4 == 0"); return SPMV_EINVAL;
+    }
+    int sm_count = 148;
+    if (device >= 0) {
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) { set_error("no CUDA device"); return SPMV_ECUDA; }
+        if (device >= ndev) { set_error("device ordinal out of range"); return SPMV_EINVAL; }
+        if ((e = cudaSetDevice(device))) return cuda_status(e, "cudaSetDevice");
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device);
+    }
+    Prepared P;
+    spmv_status st = prepare(n_rows, n_cols, nnz, row_ptr, col, val, opt.pattern != 0, P);
+    if (st) return st;
+    BuildParams bp;
+    std::vector<double> pred;
+    st = choose_params(P, opt, sm_count, bp, pred);
+    if (st) return st;
+    spmv_plan_s* p = new spmv_plan_s();
+    p->n_rows = n_rows; p->n_cols = n_cols; p->nnz = nnz; p->pattern = opt.pattern != 0;
+    p->device = device; p->opt = opt; p->sm_count = sm_count;
+    p->opt.workload_sizes = nullptr; p->opt.perf_table_path = nullptr;
+    st = pack_layout(P, bp, p->L);
+    if (st) { delete p; return st; }
+    p->perm = std::move(P.perm);
+    p->host_valid = true;
+    p->num_tiles = bp.num_tiles; p->tile_width = bp.tile_width;
+    p->tiles = p->L.tiles;
+    p->n_workloads = (int64_t)p->L.desc.size();
+    p->n_slots = (int64_t)p->L.slot_col.size();
+    p->n_row_entries = (int64_t)p->L.row_id.size();
+    p->n_split = (int64_t)p->L.split.size() / 3;
+    p->n_chunks = p->L.n_chunks;
+    predict_plan(*p, pred);
+    for (int32_t t = 0; t < p->num_tiles; ++t)
+        p->tiles[t].staged = (opt.stage_x != 0) && (p->tiles[t].col_hi - p->tiles[t].col_lo) * 4 <= 227 * 1024;
+    if (device >= 0) {
+        cudaError_t e;
+        int64_t& b = p->device_bytes;
+        if ((e = upload(&p->d_desc, p->L.desc, b)) || (e = upload(&p->d_row_id, p->L.row_id, b)) ||
+            (e = upload(&p->d_col, p->L.slot_col, b)) || (e = upload(&p->d_perm, p->perm, b)) ||
+            (e = upload(&p->d_split, p->L.split, b))) {
+            free_device(p); delete p; return cuda_status(e, "plan upload");
+        }
+        if (!p->pattern && (e = upload(&p->d_val, p->L.slot_val, b))) {
+            free_device(p); delete p; return cuda_status(e, "plan upload");
+        }
+        std::vector<float> zf(std::max<int64_t>(p->n_chunks, 1), 0.0f);
+        std::vector<int32_t> zi(std::max<int64_t>(p->n_split, 1), 0);
+        std::vector<float> xpz(p->n_cols + 4, 0.0f);
+        if ((e = upload(&p->d_partials, zf, b)) || (e = upload(&p->d_counters, zi, b)) ||
+            (e = upload(&p->d_xp, xpz, b))) {
+            free_device(p); delete p; return cuda_status(e, "plan upload");
+        }
+        if ((e = setup_grids<EpiStore>(*p, p->grid_tile))) {
+            free_device(p); delete p; return cuda_status(e, "occupancy");
+        }
+        // release the host copy (fetched back on demand by spmv_plan_layout / to_coo)
+        p->L.desc = {}; p->L.row_id = {}; p->L.slot_col = {}; p->L.slot_val = {}; p->L.split = {};
+        p->host_valid = false;
+    }
+    p->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    *out = p;
+    return SPMV_OK;
+}
+
+static spmv_status ensure_host(spmv_plan_s* p) {
+    if (p->host_valid) return SPMV_OK;
+    cudaSetDevice(p->device);
+    cudaError_t e;
+    if ((e = download(p->L.desc, p->d_desc, p->n_workloads)) ||
+        (e = download(p->L.row_id, p->d_row_id, p->n_row_entries)) ||
+        (e = download(p->L.slot_col, p->d_col, p->n_slots)) ||
+        (e = download(p->L.split, p->d_split, 3 * p->n_split)))
+        return cuda_status(e, "layout download");
+    if (!p->pattern && (e = download(p->L.slot_val, p->d_val, p->n_slots)))
+        return cuda_status(e, "layout download");
+    p->host_valid = true;
+    return SPMV_OK;
+}
+
+spmv_status execute_permuted(spmv_plan_s* p, const float* xp, float* y, cudaStream_t st) {
+    return cuda_status(launch_tiles(*p, p->grid_tile, xp, EpiStore{y}, st), "tile launch");
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+extern "C" {
+
+__attribute__((visibility("default"))) void spmv_options_default(spmv_options* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->tile_width = 0; o->num_tiles = -1; o->workload_size = -1; o->workload_sizes = nullptr;
+    o->align_rm = 8; o->split_long_rows = 1; o->camping_pad = 0; o->pattern = 0; o->ell_h = 32;
+    o->stage_x = 1; o->perf_table_path = nullptr;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_plan_create(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                             const int32_t* col_idx, const float* val, const spmv_options* opt,
+                             int device, spmv_plan* out) {
+    if (!out) { set_error("out is NULL"); return SPMV_EINVAL; }
+    *out = nullptr;
+    try {
+        return create_plan(n_rows, n_cols, nnz, row_ptr, col_idx, val, opt, device, out);
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed"); return SPMV_ENOMEM;
+    } catch (const std::exception& ex) {
+        set_error(ex.what()); return SPMV_EINVAL;
+    }
+}
+
+__attribute__((visibility("default"))) void spmv_plan_destroy(spmv_plan p) {
+    if (!p) return;
+    free_device(p);
+    delete p;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_execute_permuted(spmv_plan p, const float* xp, float* y, void* stream) {
+    if (!p || !xp || !y) { set_error("null argument"); return SPMV_EINVAL; }
+    if (p->device < 0) { set_error("host-only plan cannot execute"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    return execute_permuted(p, xp, y, (cudaStream_t)stream);
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_execute(spmv_plan p, const float* x, float* y, void* stream) {
+    if (!p || !x || !y) { set_error("null argument"); return SPMV_EINVAL; }
+    if (p->device < 0) { set_error("host-only plan cannot execute"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->n_cols > 0) {
+        int grid = (int)std::min<int64_t>((p->n_cols + 255) / 256, (int64_t)p->sm_count * 8);
+        permute_x_kernel<<<grid, 256, 0, st>>>(x, p->d_perm, p->d_xp, p->n_cols);
+        if ((e = cudaGetLastError())) return cuda_status(e, "permute_x");
+    }
+    return execute_permuted(p, p->d_xp, y, st);
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_execute_host(spmv_plan p, const float* xh, float* yh, void* stream) {
+    if (!p || !xh || !yh) { set_error("null argument"); return SPMV_EINVAL; }
+    if (p->device < 0) { set_error("host-only plan cannot execute"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    float *dx = nullptr, *dy = nullptr;
+    if ((e = cudaMallocAsync(&dx, std::max<int64_t>(p->n_cols, 1) * 4, st)) ||
+        (e = cudaMallocAsync(&dy, std::max<int64_t>(p->n_rows, 1) * 4, st)))
+        return cuda_status(e, "cudaMallocAsync");
+    spmv_status s = SPMV_OK;
+    if ((e = cudaMemcpyAsync(dx, xh, p->n_cols * 4, cudaMemcpyHostToDevice, st))) s = cuda_status(e, "H2D");
+    if (!s) s = spmv_execute(p, dx, dy, stream);
+    if (!s && (e = cudaMemcpyAsync(yh, dy, p->n_rows * 4, cudaMemcpyDeviceToHost, st))) s = cuda_status(e, "D2H");
+    cudaFreeAsync(dx, st); cudaFreeAsync(dy, st);
+    if (!s && (e = cudaStreamSynchronize(st))) s = cuda_status(e, "sync");
+    return s;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_execute_timed(spmv_plan p, const float* x, float* y, void* stream,
+                               float* launch_ms, int32_t max_launches) {
+    if (!p || !x || !y || !launch_ms) { set_error("null argument"); return SPMV_EINVAL; }
+    if (p->device < 0) { set_error("host-only plan cannot execute"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<cudaEvent_t> ev;
+    auto mark = [&]() { cudaEvent_t v; cudaEventCreate(&v); cudaEventRecord(v, st); ev.push_back(v); };
+    mark();
+    if (p->n_cols > 0) {
+        int grid = (int)std::min<int64_t>((p->n_cols + 255) / 256, (int64_t)p->sm_count * 8);
+        permute_x_kernel<<<grid, 256, 0, st>>>(x, p->d_perm, p->d_xp, p->n_cols);
+        mark();
+    }
+    for (int32_t t = 0; t <= p->num_tiles; ++t) {
+        if (p->tiles[t].wl_end == p->tiles[t].wl_begin) continue;
+        if ((e = launch_tile(*p, t, p->grid_tile[t], p->d_xp, EpiStore{y}, st))) break;
+        mark();
+    }
+    if (!e) e = cudaStreamSynchronize(st);
+    for (size_t i = 1; i < ev.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+        if ((int32_t)(i - 1) < max_launches) launch_ms[i - 1] = ms;
+    }
+    for (auto v : ev) cudaEventDestroy(v);
+    return cuda_status(e, "spmv_execute_timed");
+}
+
+__attribute__((visibility("default")))
+int32_t spmv_plan_launches(spmv_plan p) {
+    if (!p) return 0;
+    int32_t n = p->n_cols > 0 ? 1 : 0;
+    for (auto& t : p->tiles) n += (t.wl_end > t.wl_begin) ? 1 : 0;
+    return n;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_plan_stats(spmv_plan p, spmv_plan_stats_t* o) {
+    if (!p || !o) { set_error("null argument"); return SPMV_EINVAL; }
+    std::memset(o, 0, sizeof(*o));
+    o->n_rows = p->n_rows; o->n_cols = p->n_cols; o->nnz = p->nnz;
+    o->num_tiles = p->num_tiles; o->tile_width = p->tile_width;
+    o->n_workloads = p->n_workloads; o->n_slots = p->n_slots; o->n_row_entries = p->n_row_entries;
+    o->n_split = p->n_split; o->n_chunks = p->n_chunks; o->device_bytes = p->device_bytes;
+    o->predicted_us = p->predicted_us; o->build_ms = p->build_ms;
+    for (int32_t t = 0; t <= p->num_tiles && t < 64; ++t) {
+        const TileInfo& ti = p->tiles[t];
+        o->wl[t] = ti.wl; o->tile_nnz[t] = ti.nnz; o->tile_rows[t] = ti.rows;
+        o->tile_col_lo[t] = ti.col_lo; o->tile_col_hi[t] = ti.col_hi; o->tile_staged[t] = ti.staged;
+        o->tile_predicted_us[t] = ti.pred_us; o->composite_threshold[t] = ti.threshold;
+    }
+    return SPMV_OK;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_plan_layout(spmv_plan p, spmv_layout_view* v) {
+    if (!p || !v) { set_error("null argument"); return SPMV_EINVAL; }
+    spmv_status s = ensure_host(p);
+    if (s) return s;
+    HostLayout& L = p->L;
+    const int64_t nw = p->n_workloads;
+    L.v_tiles.resize(4 * (p->num_tiles + 1));
+    for (int32_t t = 0; t <= p->num_tiles; ++t) {
+        L.v_tiles[4 * t] = p->tiles[t].col_lo; L.v_tiles[4 * t + 1] = p->tiles[t].col_hi;
+        L.v_tiles[4 * t + 2] = p->tiles[t].wl_begin; L.v_tiles[4 * t + 3] = p->tiles[t].wl_end;
+    }
+    L.v_off.resize(nw); L.v_row_base.resize(nw); L.v_w.resize(nw); L.v_h.resize(nw);
+    L.v_split_id.resize(nw); L.v_chunk.resize(nw); L.v_kind.resize(nw); L.v_kvec.resize(nw);
+    for (int64_t j = 0; j < nw; ++j) {
+        const WlDesc& d = L.desc[j];
+        L.v_off[j] = d.off; L.v_row_base[j] = d.row_base; L.v_w[j] = d.w; L.v_h[j] = d.h;
+        L.v_split_id[j] = d.split_id; L.v_chunk[j] = d.chunk; L.v_kind[j] = d.kind; L.v_kvec[j] = d.kvec;
+    }
+    v->n_cols = p->n_cols; v->n_workloads = nw; v->n_row_entries = p->n_row_entries;
+    v->n_slots = p->n_slots; v->n_split = p->n_split; v->n_tiles_total = p->num_tiles + 1;
+    v->perm = p->perm.data(); v->tiles = L.v_tiles.data();
+    v->desc_off = L.v_off.data(); v->desc_row_base = L.v_row_base.data(); v->desc_w = L.v_w.data();
+    v->desc_h = L.v_h.data(); v->desc_split_id = L.v_split_id.data(); v->desc_chunk = L.v_chunk.data();
+    v->desc_kind = L.v_kind.data(); v->desc_kvec = L.v_kvec.data();
+    v->row_id = L.row_id.data(); v->slot_col = L.slot_col.data();
+    v->slot_val = p->pattern ? nullptr : L.slot_val.data();
+    v->split = L.split.data();
+    return SPMV_OK;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_plan_to_coo(spmv_plan p, int32_t* rows, int32_t* cols, float* vals) {
+    if (!p || (p->nnz > 0 && (!rows || !cols))) { set_error("null argument"); return SPMV_EINVAL; }
+    spmv_status s = ensure_host(p);
+    if (s) return s;
+    const HostLayout& L = p->L;
+    const int64_t eh = p->opt.ell_h;
+    int64_t w = 0;
+    for (int32_t t = 0; t <= p->num_tiles; ++t) {
+        const TileInfo& ti = p->tiles[t];
+        const int32_t sent = (int32_t)(ti.col_hi - ti.col_lo);
+        for (int64_t j = ti.wl_begin; j < ti.wl_end; ++j) {
+            const WlDesc& d = L.desc[j];
+            auto put = [&](uint32_t ent, int64_t slot) {
+                int32_t c = L.slot_col[slot];
+                if (c == sent) return;
+                if (w >= p->nnz) return;
+                rows[w] = (int32_t)(ent & ROW_MASK);
+                cols[w] = p->perm[ti.col_lo + c];
+                if (vals) vals[w] = p->pattern ? 1.0f : L.slot_val[slot];
+                ++w;
+            };
+            if (d.kind != KIND_CM) {
+                for (int32_t r = 0; r < d.h; ++r)
+                    for (int32_t k = 0; k < d.w; ++k) put(L.row_id[d.row_base + r], d.off + (int64_t)r * d.w + k);
+            } else {
+                for (int32_t r = 0; r < d.h; ++r) {
+                    uint32_t ent = L.row_id[d.row_base + r];
+                    if (ent == PAD_ROW) continue;
+                    int64_t s0 = d.off + (int64_t)(r / eh) * eh * d.w, rr = r % eh;
+                    for (int32_t k = 0; k < d.w; ++k)
+                        put(ent, s0 + (k / d.kvec) * eh * d.kvec + rr * d.kvec + (k % d.kvec));
+                }
+            }
+        }
+    }
+    if (w != p->nnz) { set_error("layout decode count mismatch"); return SPMV_EINVAL; }
+    return SPMV_OK;
+}
+
+__attribute__((visibility("default"))) const char* spmv_last_error(void) { return g_last_error.c_str(); }
+__attribute__((visibility("default"))) const char* spmv_version(void) { return "tcspmv 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// plan_impl.h -- the plan object behind spmv_plan, and the tile launcher shared by
+// spmv_execute and the power iterations.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "plan.h"
+
+struct spmv_plan_s {
+    int64_t n_rows = 0, n_cols = 0, nnz = 0;
+    bool pattern = false;
+    int device = -1;
+    spmv_options opt{};
+    tc::HostLayout L;              // host copy (kept for host-only plans; fetched on demand)
+    bool host_valid = false;
+    std::vector<int32_t> perm;
+    int32_t num_tiles = 0, tile_width = 0;
+    int64_t n_workloads = 0, n_slots = 0, n_row_entries = 0, n_split = 0, n_chunks = 0;
+    std::vector<tc::TileInfo> tiles;
+    double predicted_us = 0.0, build_ms = 0.0;
+    // device
+    tc::WlDesc* d_desc = nullptr;
+    uint32_t* d_row_id = nullptr;
+    int32_t* d_col = nullptr;
+    float* d_val = nullptr;
+    int32_t* d_perm = nullptr;
+    float* d_xp = nullptr;          // relabelled x for spmv_execute
+    int32_t* d_split = nullptr;
+    float* d_partials = nullptr;
+    int32_t* d_counters = nullptr;
+    int64_t device_bytes = 0;
+    int sm_count = 0;
+    std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
+};
+
+namespace tc {
+spmv_status cuda_status(cudaError_t e, const char* what);
+}  // namespace tc

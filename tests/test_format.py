@@ -1,0 +1,141 @@
+"""CPU tests of the C-ABI library (no GPU): every symbol of include/spmv.h is exported, and the
+product builder's layout is byte-identical to the independent numpy format oracle
+(oracle/format_ref.py) on the same explicit parameters; layout -> COO equals the input."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import graphgen
+from oracle import format_ref
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1103_2405_b200 import _capi
+    hdr = open(os.path.join(ROOT, "include", "spmv.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = set(re.findall(r"\b([a-z_][a-z0-9_]*)\s*\(", hdr))
+    names -= {"if", "sizeof", "defined"}
+    lib = ctypes.CDLL(_capi.LIB_PATH)
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(names) == set(_capi.SIGNATURES), set(names) ^ set(_capi.SIGNATURES)
+    assert _capi.lib().spmv_version().startswith(b"tcspmv")
+
+
+def build_both(nr, nc, rp, col, val, tw, T, wls, align=8, split=True, camping=False, ell_h=32):
+    from paper_1103_2405_b200 import Plan
+    ref = format_ref.build(nr, nc, rp, col, val, tw, T, wls, align_rm=align, split_long_rows=split,
+                           camping_pad=camping, ell_h=ell_h)
+    p = Plan(nr, nc, rp, col, val, device=-1, tile_width=tw, num_tiles=T, workload_sizes=wls,
+             align_rm=align, split_long_rows=int(split), camping_pad=int(camping), ell_h=ell_h,
+             pattern=int(val is None))
+    return ref, p
+
+
+def assert_same(ref, p):
+    L = p.layout()
+    assert np.array_equal(L["perm"], ref.perm)
+    assert np.array_equal(L["tiles"], ref.tiles)
+    for k in ("off", "row_base", "w", "h", "kind", "kvec", "split_id", "chunk"):
+        assert np.array_equal(L["desc"][k], ref.desc[k]), k
+    assert np.array_equal(L["row_id"], ref.row_id)
+    assert np.array_equal(L["slot_col"], ref.slot_col)
+    if ref.slot_val is None:
+        assert L["slot_val"] is None
+    else:
+        assert L["slot_val"].tobytes() == ref.slot_val.tobytes()
+    assert np.array_equal(L["split"].reshape(-1, 3), ref.split.reshape(-1, 3))
+
+
+def test_fig1_fixture_bit_exact():
+    with open(os.path.join(ROOT, "tests", "golden", "fig1.json")) as f:
+        g = json.load(f)
+    ents = sorted(map(tuple, g["entries_row_col"]))
+    rp = np.zeros(g["n_rows"] + 1, np.int64)
+    for r, _ in ents:
+        rp[r + 1] += 1
+    rp = np.cumsum(rp)
+    col = np.array([c for _, c in ents], np.int32)
+    ref, p = build_both(8, 8, rp, col, None, 2, 2, [4, 4, 4], align=2, ell_h=2)
+    assert_same(ref, p)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_bit_exact(seed):
+    rng = np.random.default_rng(1000 + seed)
+    nr, nc = int(rng.integers(1, 600)), int(rng.integers(1, 600))
+    kind = "powerlaw" if seed % 2 else "uniform"
+    valued = seed % 3 != 0
+    rp, col, val = graphgen.random_csr(nr, nc, int(rng.integers(0, 6000)), seed=seed, kind=kind,
+                                       valued=valued, signed=bool(seed % 4 == 1))
+    tw = int(rng.integers(1, 64))
+    maxT = (nc + tw - 1) // tw
+    T = int(rng.integers(0, min(maxT, 5) + 1))
+    wls = [int(rng.integers(1, 300)) for _ in range(T + 1)]
+    ref, p = build_both(nr, nc, rp, col, val, tw, T, wls, align=[4, 8, 32][seed % 3],
+                        split=seed % 5 != 0 or True, camping=seed % 4 == 2)
+    assert_same(ref, p)
+    r, c, v = p.to_coo()
+    got = sorted(zip(r.tolist(), c.tolist(), v.tolist()))
+    exp_v = np.ones(len(col), np.float32) if val is None else val
+    exp = sorted(zip(np.repeat(np.arange(nr), np.diff(rp)).tolist(), col.tolist(), exp_v.tolist()))
+    assert got == exp
+
+
+def test_graph_bit_exact_t_small():
+    G = graphgen.make_graph("t_small")
+    # PageRank's matrix is A^T (rows = targets)
+    rpt, colt = graphgen.keys_to_csr(G.keys, G.n, transpose=True)
+    ref, p = build_both(G.n, G.n, rpt, colt, None, 256, 3, [64, 128, 32, 512])
+    assert_same(ref, p)
+
+
+def test_paper_mode_rowsplit_error():
+    from paper_1103_2405_b200 import Plan, SpmvError
+    rp = np.array([0, 10, 11])
+    col = np.concatenate([np.arange(10), [3]]).astype(np.int32)
+    with pytest.raises(SpmvError, match="EROWSPLIT"):
+        Plan(2, 10, rp, col, None, device=-1, tile_width=10, num_tiles=0, workload_sizes=[4],
+             split_long_rows=0)
+    Plan(2, 10, rp, col, None, device=-1, tile_width=10, num_tiles=0, workload_sizes=[10],
+         split_long_rows=0)
+
+
+@pytest.mark.parametrize("bad", ["rowptr", "col", "nrows"])
+def test_invalid_inputs(bad):
+    from paper_1103_2405_b200 import Plan, SpmvError
+    rp = np.array([0, 2, 3]); col = np.array([0, 1, 1], np.int32)
+    if bad == "rowptr":
+        rp = np.array([0, 3, 2])
+    if bad == "col":
+        col = np.array([0, 5, 1], np.int32)
+    with pytest.raises(SpmvError, match="EINVAL"):
+        if bad == "nrows":
+            Plan(-1, 2, rp, col, None, device=-1)
+        else:
+            Plan(2, 2, rp, col, None, device=-1)
+
+
+def test_empty_matrix_and_zero_rows():
+    from paper_1103_2405_b200 import Plan
+    ref, p = build_both(5, 3, np.zeros(6, np.int64), np.zeros(0, np.int32), None, 2, 0, [16])
+    assert_same(ref, p)
+    L = p.layout()
+    assert L["desc"]["w"].tolist() == [0] and L["desc"]["h"].tolist() == [32]
+    rows = [int(e) & ((1 << 29) - 1) for e in L["row_id"] if e != 0xFFFFFFFF]
+    assert rows == [0, 1, 2, 3, 4]
+
+
+def test_no_device_means_loud_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has GPU")
+    from paper_1103_2405_b200 import Plan, SpmvError
+    with pytest.raises(SpmvError, match="ECUDA"):
+        Plan(2, 2, np.array([0, 1, 2]), np.array([1, 0], np.int32), None, device=0)

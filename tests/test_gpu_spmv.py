@@ -1,0 +1,106 @@
+"""GPU parity of the tiled-composite SpMV (through the C ABI) against the fp64 oracle.
+Bar (BASELINE.json north_star): |y - y_ref| <= 1e-5 * sum_j |a_ij x_j| + 1e-30 per element."""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+def run_plan(nr, nc, rp, col, val, x, **opt):
+    import torch
+    from paper_1103_2405_b200 import Plan
+    p = Plan(nr, nc, rp, col, val, device=0, **opt)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    yt = torch.full((max(nr, 1),), float("nan"), device="cuda")
+    p.execute(xt, yt)
+    torch.cuda.synchronize()
+    return p, yt.cpu().numpy()[:nr]
+
+
+def check(y, rp, col, val, x):
+    yref, b = oracle.spmv(rp, col, val, x)
+    err = np.abs(y.astype(np.float64) - yref)
+    bad = err > RTOL * b + 1e-30
+    assert not bad.any(), f"{bad.sum()} rows off; worst {err[bad][:5]} vs bound {(RTOL * b)[bad][:5]}"
+
+
+CASES = [
+    # (nr, nc, nnz, kind, valued, signed, options)
+    (300, 200, 3000, "uniform", True, False, dict(tile_width=16, num_tiles=3, workload_size=64)),
+    (1000, 1000, 20000, "powerlaw", True, True, dict(tile_width=64, num_tiles=4, workload_size=128)),
+    (1000, 1000, 20000, "powerlaw", False, False, dict(tile_width=64, num_tiles=4, workload_size=128)),
+    (777, 3001, 40000, "powerlaw", True, False, dict(tile_width=100, num_tiles=2, workload_sizes=[37, 512, 1000])),
+    (5000, 300, 60000, "uniform", True, True, dict(tile_width=300, num_tiles=1, workload_size=4096)),
+    (2000, 2000, 50000, "powerlaw", True, False, dict(tile_width=512, num_tiles=2, workload_size=96, stage_x=0)),
+    (2000, 2000, 50000, "powerlaw", True, False, dict(tile_width=512, num_tiles=2, workload_size=96, align_rm=32)),
+    (2000, 2000, 50000, "powerlaw", True, False, dict(tile_width=512, num_tiles=2, workload_size=96, camping_pad=1)),
+    (3000, 3000, 90000, "powerlaw", True, False, dict(num_tiles=0, split_long_rows=0)),
+    (3000, 3000, 90000, "powerlaw", True, False, dict()),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_spmv_parity_random(case, gpu):
+    nr, nc, nnz, kind, valued, signed, opt = CASES[case]
+    rp, col, val = graphgen.random_csr(nr, nc, nnz, seed=case, kind=kind, valued=valued, signed=signed)
+    x = graphgen.uniform_f32(nc, seed=3, mode=2 if signed else 0)
+    if not valued:
+        opt = dict(opt, pattern=1)
+    p, y = run_plan(nr, nc, rp, col, val, x, **opt)
+    check(y, rp, col, val, x)
+
+
+def test_edge_cases(gpu):
+    # nnz = 0 (empty rows are written as 0, never left stale)
+    p, y = run_plan(7, 5, np.zeros(8, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32),
+                    np.ones(5, np.float32))
+    assert (y == 0).all()
+    # 1x1
+    p, y = run_plan(1, 1, np.array([0, 1]), np.array([0], np.int32), np.array([2.5], np.float32),
+                    np.array([4.0], np.float32))
+    assert y.tolist() == [10.0]
+    # one full row, far longer than WL: split into chunks, combined in chunk order
+    n = 100_003
+    rp = np.array([0, n, n + 1])
+    col = np.concatenate([np.arange(n), [7]]).astype(np.int32)
+    val = graphgen.uniform_f32(n + 1, seed=9, mode=2)
+    x = graphgen.uniform_f32(n, seed=10, mode=2)
+    p, y = run_plan(2, n, rp, col, val, x, workload_size=1000, tile_width=4096, num_tiles=3)
+    check(y, rp, col, val, x)
+    assert p.stats()["n_split"] >= 1
+    # all rows of length 1, identity and permutation matrices are exact
+    m = 4099
+    perm = np.random.default_rng(0).permutation(m).astype(np.int32)
+    x = graphgen.uniform_f32(m, seed=11, mode=2)
+    p, y = run_plan(m, m, np.arange(m + 1), perm, np.ones(m, np.float32), x, tile_width=1024, num_tiles=2)
+    assert np.array_equal(y, x[perm])
+    # rectangular with empty columns and rows; signed values
+    rp, col, val = graphgen.random_csr(50, 9000, 700, seed=4, signed=True)
+    x = graphgen.uniform_f32(9000, seed=12, mode=2)
+    p, y = run_plan(50, 9000, rp, col, val, x, tile_width=2048, num_tiles=2, workload_size=8)
+    check(y, rp, col, val, x)
+
+
+def test_graph_auto_and_deterministic(gpu):
+    import torch
+    from paper_1103_2405_b200 import Plan
+    G = graphgen.make_graph("t_mid")
+    rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)
+    val = graphgen.edge_values(G.keys[np.lexsort((G.keys >> np.uint64(32), G.keys & np.uint64(0xFFFFFFFF)))])
+    x = graphgen.uniform_f32(G.n, seed=3)
+    for opt in (dict(), dict(tile_width=8192, num_tiles=4, workload_size=512)):
+        p = Plan(G.n, G.n, rp, col, val, device=0, **opt)
+        xt = torch.from_numpy(x).cuda()
+        y1 = torch.empty(G.n, device="cuda"); y2 = torch.empty(G.n, device="cuda")
+        p.execute(xt, y1); p.execute(xt, y2)
+        torch.cuda.synchronize()
+        a, b = y1.cpu().numpy(), y2.cpu().numpy()
+        assert a.tobytes() == b.tobytes()            # bitwise run-to-run
+        check(a, rp, col, val, x)
+        yh = p.execute_host(x)                       # host path through the C ABI
+        assert yh.tobytes() == a.tobytes()
