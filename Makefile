@@ -48,3 +48,9 @@ clean:
 	rm -rf build graphgen/*.so oracle/*.so $(LIBDIR)
 
 .PHONY: all clean
+
+# experiment builds (not used by the product path): kernel-shape variants, make expvar V=name F="-D..."
+expvar:
+	@mkdir -p build_$(V) $(LIBDIR)
+	for f in $(CU_SRCS); do $(NVCC) $(NVFLAGS) $(F) -c $$f -o build_$(V)/$$(basename $$f).o 2>/dev/null || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $(LIBDIR)/libtcspmv_$(V).so build_$(V)/*.cu.o $(CPP_OBJS) -Xcompiler -fopenmp -lcudart_static -ldl -lpthread -lrt

@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): LiveJournal-shaped R-MAT graph,
+n = 4,847,571 vertices, m = 68,993,773 edges, valued (edge values U(0,1]), fp32.
+Step: one tiled-composite SpMV y = A x through spmv_execute (x permutation + every tile launch),
+inputs resident in HBM.  Metric: SpMV GFLOP/s (= 2 m / step time); HBM GB/s and the PageRank /
+HITS / RWR iteration rates on the same graph are reported beside it.
+N > 1 (torchrun): every rank runs its own replica of the workload (independent problems, no
+data-path collective): weak scaling, value = total flops of all ranks / max-over-ranks time.
+`--impl reference` times the fp64 CPU oracle (the only reference this paper-only tier has).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMV GFLOP/s and HBM GB/s vs 8 TB/s; PageRank iters/s at 1/2/4/8 B200"
+WORKLOAD = "c2: LiveJournal-shaped R-MAT s23 (a,b,c,d)=(.50,.20,.20,.10), n=4847571, m=68993773, valued fp32"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self.stop = index, [], threading.Event()
+        self.marks = []
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                self.samples.append((time.time(), out))
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self, t0, t1):
+        rows = [s for (t, s) in self.samples if t0 <= t <= t1] or [s for (_, s) in self.samples]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[0])); mx = max(mx, float(f[1]))
+                for i, nm in enumerate(names):
+                    if f[2 + i].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_workload():
+    import graphgen
+    G = graphgen.make_graph("c2")
+    val = graphgen.edge_values(G.keys, seed=graphgen.SEED_VAL, mode=1)
+    x = graphgen.uniform_f32(G.n, seed=graphgen.SEED_X)
+    return G, val, x
+
+
+def reference_arm(args):
+    """fp64 CPU oracle, as it stands, on this box's host cores."""
+    import oracle
+    G, val, x = load_workload()
+    oracle.spmv(G.row_ptr, G.col, val, x)        # warm (page-in)
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle.spmv(G.row_ptr, G.col, val, x)
+    steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.spmv(G.row_ptr, G.col, val, x)
+    dt = (time.perf_counter() - t0) / steps
+    v = 2.0 * G.m / dt / 1e9
+    cores = len(os.sched_getaffinity(0))
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GFLOP/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": f"full c2 SpMV x {steps} (fp64 CSR, OpenMP over rows)"},
+            "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip PageRank/HITS/RWR and cpu_baseline")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import graphgen
+    import oracle
+    import paper_1103_2405_b200 as pkg
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G, val, x = load_workload()
+    plan = pkg.Plan(G.n, G.n, G.row_ptr, G.col, val, device=local)
+    st = plan.stats()
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.empty(G.n, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # parity gate on sampled rows (the oracle computes them one by one)
+    plan.execute(xt, yt)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(rank).choice(G.n, size=2000, replace=False)
+    rows = np.unique(np.concatenate([rows, np.argsort(np.diff(G.row_ptr))[-50:]]))
+    sub_rp = np.concatenate([[0], np.cumsum(np.diff(G.row_ptr)[rows])]).astype(np.int64)
+    idx = np.concatenate([np.arange(G.row_ptr[r], G.row_ptr[r + 1]) for r in rows])
+    yref, b = oracle.spmv(sub_rp, G.col[idx], val[idx], x)
+    y = yt.cpu().numpy()[rows].astype(np.float64)
+    parity_ok = bool((np.abs(y - yref) <= 1e-5 * b + 1e-30).all())
+
+    for _ in range(args.warmup):
+        plan.execute(xt, yt)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        # ~1 s soak so the clock sampler sees the kernel under load
+        t_soak = time.time()
+        while time.time() - t_soak < 1.0:
+            for _ in range(50):
+                plan.execute(xt, yt)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.execute(xt, yt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * 2.0 * G.m / (ms * 1e-3) / 1e9
+    alg_bytes = 8 * G.m + 12 * G.n
+    hbm_gbs = alg_bytes / (ms * 1e-3) / 1e9
+
+    # per-launch device times (CUDA events between launches on the same stream)
+    nl = plan.launches
+    per = np.zeros(nl, np.float64)
+    buf = (np.zeros(nl, np.float32))
+    reps = max(10, args.steps // 10)
+    import ctypes
+    for _ in range(reps):
+        pkg._capi.check(pkg.lib().spmv_execute_timed(plan._h, ctypes.c_void_p(xt.data_ptr()),
+                                                      ctypes.c_void_p(yt.data_ptr()),
+                                                      ctypes.c_void_p(stream.cuda_stream),
+                                                      buf.ctypes.data, nl), "spmv_execute_timed")
+        per += buf
+    per /= reps
+    # launch 0 = x permutation (12 B per column), then the non-empty tiles in order
+    tiles = [t for t in range(st["num_tiles"] + 1) if st["tile_nnz"][t] > 0 or t == st["num_tiles"]]
+    launch_bytes = [12.0 * G.n]
+    launch_names = ["permute_x"]
+    for t in tiles[: nl - 1]:
+        width = st["tile_col_hi"][t] - st["tile_col_lo"][t]
+        launch_bytes.append(8.0 * st["tile_nnz"][t] + 8.0 * st["tile_rows"][t] + 4.0 * width)
+        launch_names.append(f"tc_spmv_tile[{t}]" + ("(smem x)" if st["tile_staged"][t] else "(L1/L2 x)"))
+    dom = int(np.argmax(per))
+    peak, peak_src = peaks()
+    ach = launch_bytes[dom] / (per[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "kernel": launch_names[dom],
+                "kernel_share": round(float(per[dom] / per.sum()), 3), "peak_source": peak_src,
+                "per_launch_us": [round(float(v) * 1e3, 2) for v in per],
+                "launch_names": launch_names}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(launch_names[dom].split("(")[0])
+            if tr:
+                roofline["traffic"] = tr
+    except Exception:
+        pass
+
+    # end to end through the public API with host buffers (H2D x, D2H y inside every step)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty(G.n, dtype=torch.float32).pin_memory()
+    e2e_steps = max(5, args.steps // 10)
+    for _ in range(2):
+        pkg._capi.check(pkg.lib().spmv_execute_host(plan._h, ctypes.c_void_p(xh.data_ptr()),
+                                                     ctypes.c_void_p(yh.data_ptr()),
+                                                     ctypes.c_void_p(stream.cuda_stream)), "e2e")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        pkg._capi.check(pkg.lib().spmv_execute_host(plan._h, ctypes.c_void_p(xh.data_ptr()),
+                                                     ctypes.c_void_p(yh.data_ptr()),
+                                                     ctypes.c_void_p(stream.cuda_stream)), "e2e")
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e = {"value": round(world * 2.0 * G.m / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+           "h2d_bytes_per_step": 4 * G.n, "d2h_bytes_per_step": 4 * G.n,
+           "ms_per_step": round(e2e_ms, 4)}
+
+    extras, cpu = {}, None
+    if rank == 0 and world == 1 and not args.no_extras:
+        for algo in ("pagerank", "hits", "rwr"):
+            s = pkg.Solver(algo, G.n, G.row_ptr, G.col, device=local)
+            q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][0]) if algo == "rwr" else 0
+            s.run(q)
+            info = s.run(q)
+            extras[f"{algo}_iters_per_s"] = round(1e3 * info["iterations"] / info["ms_total"], 1)
+            extras[f"{algo}_iterations"] = info["iterations"]
+            extras[f"{algo}_us_per_iter"] = round(info["us_per_iter"], 2)
+            s.close()
+        # cpu_baseline: the oracle as it stands on this box's host cores, bounded sample
+        oracle.spmv(G.row_ptr, G.col, val, x)
+        reps_cpu, tc0 = 0, time.perf_counter()
+        while time.perf_counter() - tc0 < 10.0:
+            oracle.spmv(G.row_ptr, G.col, val, x)
+            reps_cpu += 1
+        dtc = (time.perf_counter() - tc0) / reps_cpu
+        cpu = {"value": round(2.0 * G.m / dtc / 1e9, 3), "unit": "GFLOP/s",
+               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"full c2 SpMV repeated {reps_cpu}x over ~10 s (fp64 CSR, OpenMP over rows)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (0.57 GB of col/val streamed per step); x (19 MB) L2-resident",
+                       "plan": {k: st[k] for k in ("num_tiles", "tile_width", "wl", "tile_staged",
+                                                     "n_workloads", "n_slots")}},
+            "hbm_GBps_algorithmic": round(hbm_gbs, 1),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(args.steps * nl),
+            "clocks": clk.summary(t0, t1),
+            "parity_sampled_rows_ok": parity_ok,
+            "predicted_us": round(st["predicted_us"], 2),
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

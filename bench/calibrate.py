@@ -1,0 +1,129 @@
+"""Offline performance table of the tiled-composite kernels on this GPU (Sec. 3.3:
+"we artificially construct a matrix in tile-composite format, in which all workloads are set to
+the same w by h shape and there are large number of such workloads").
+
+For every sampled shape (kind, w, h), x mode (cached = the tile's x segment staged in shared
+memory, uncached = gathers through L1/L2 from a c2-sized x, L160) and value type, a synthetic
+matrix whose packing yields only that shape is built through the C ABI, the tile launch is timed
+with CUDA events (spmv_execute_timed), and whole-GPU slots/s is recorded (reading R20).
+
+Writes paper_1103_2405_b200/data/perf_table_b200.json, read by the auto-tuner.
+Usage (GPU box): python bench/calibrate.py [--quick]
+"""
+import ctypes
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1103_2405_b200 as pkg  # noqa: E402
+
+KIND = {"rm": 0, "cm": 1}
+N_UNCACHED = 4_847_571       # x of the LiveJournal-shaped config (L2-resident)
+TW_CACHED = 24576            # staged tile width (96 KB of x per CTA)
+
+
+def shape_matrix(kind, w, h, n_cols, target_slots, rng):
+    """rows of length w; WL = w*h makes every workload exactly (w, h)."""
+    nw = max(1, target_slots // (w * h))
+    n_rows = nw * h
+    col = rng.integers(0, n_cols, size=n_rows * w, dtype=np.int64)
+    # distinct columns inside a row keep the row length exactly w
+    if w > 1:
+        col = col.reshape(n_rows, w)
+        col = (col + np.arange(w)[None, :] * 7919) % n_cols
+        col = col.reshape(-1)
+    rp = np.arange(0, n_rows * w + 1, w, dtype=np.int64)
+    return n_rows, rp, col.astype(np.int32)
+
+
+def measure(kind, w, h, cached, valued, target_slots, reps=5):
+    rng = np.random.default_rng(w * 1000 + h)
+    n_cols = TW_CACHED if cached else N_UNCACHED
+    n_rows, rp, col = shape_matrix(kind, w, h, n_cols, target_slots, rng)
+    val = rng.uniform(0, 1, len(col)).astype(np.float32) if valued else None
+    opt = dict(tile_width=TW_CACHED if cached else n_cols, num_tiles=1 if cached else 0,
+               workload_size=w * h, align_rm=8)
+    p = pkg.Plan(n_rows, n_cols, rp, col, val, device=0, **opt)
+    st = p.stats()
+    x = torch.rand(n_cols, device="cuda")
+    y = torch.empty(n_rows, device="cuda")
+    nl = p.launches
+    buf = np.zeros(nl, np.float32)
+    times = []
+    s = torch.cuda.current_stream()
+    for r in range(reps + 1):
+        pkg._capi.check(pkg.lib().spmv_execute_timed(p._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                                      ctypes.c_void_p(s.cuda_stream), buf.ctypes.data, nl), "timed")
+        if r:
+            times.append(float(buf[1]))          # launch 1 = the first tile
+    ms = float(np.median(times))
+    slots = st["n_slots"]
+    p.close()
+    return slots / (ms * 1e-3), ms, st["resident_warps"]
+
+
+def main():
+    quick = "--quick" in sys.argv
+    target = 4_000_000 if quick else 16_000_000
+    rm_w = [8, 32, 128, 512, 2048] if quick else [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
+    rm_h = [1, 4, 16, 64] if quick else [1, 2, 4, 8, 16, 32, 64]
+    cm_w = [1, 2, 4, 8, 16, 31] if quick else [1, 2, 3, 4, 6, 8, 12, 16, 24, 31]
+    cm_h = [32, 128, 512] if quick else [32, 64, 128, 256, 512, 1024]
+    entries = []
+    t0 = time.time()
+    warps = 0
+    for valued in (True, False):
+        for cached in (False, True):
+            for w in rm_w:
+                for h in rm_h:
+                    if h > w or w * h > 32768:
+                        continue
+                    sps, ms, warps = measure("rm", w, h, cached, valued, target)
+                    entries.append([int(cached), int(valued), 0, w, h, round(sps, 1)])
+            for w in cm_w:
+                for h in cm_h:
+                    if h <= w or w * h > 32768:
+                        continue
+                    sps, ms, warps = measure("cm", w, h, cached, valued, target)
+                    entries.append([int(cached), int(valued), 1, w, h, round(sps, 1)])
+            print(f"valued={valued} cached={cached}: {len(entries)} entries, {time.time() - t0:.0f}s", flush=True)
+    # per-launch overhead: a tile with a single 32-row workload
+    rp = np.arange(0, 33, dtype=np.int64)
+    col = np.arange(32, dtype=np.int32)
+    p = pkg.Plan(32, 32, rp, col, None, device=0, num_tiles=0, workload_size=1)
+    x = torch.rand(32, device="cuda"); y = torch.empty(32, device="cuda")
+    buf = np.zeros(p.launches, np.float32)
+    lt = []
+    for r in range(20):
+        pkg._capi.check(pkg.lib().spmv_execute_timed(p._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                                      ctypes.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                                      buf.ctypes.data, p.launches), "timed")
+        if r > 2:
+            lt.append(float(buf[-1]))
+    launch_us = float(np.median(lt)) * 1e3
+    out = {"version": 1, "device": torch.cuda.get_device_name(0),
+           "sms": torch.cuda.get_device_properties(0).multi_processor_count,
+           "max_act_warp": int(warps), "launch_us": round(launch_us, 3),
+           "stage_GBps": 6000.0, "rmw_GBps": 4000.0,
+           "units": "slots per second, whole GPU, every warp on one (w,h) shape (reading R20)",
+           "columns": ["cached", "valued", "kind(0=rm,1=cm)", "w", "h", "slots_per_s"],
+           "entries": entries}
+    path = os.path.join(ROOT, "paper_1103_2405_b200", "data", "perf_table_b200.json")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump(out, f, indent=0)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "perf_table_b200.json"), "w") as f:
+        json.dump(out, f, indent=0)
+    print(json.dumps({"entries": len(entries), "launch_us": launch_us, "max_act_warp": warps,
+                      "seconds": round(time.time() - t0, 1)}))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,4 @@
+python -m pytest tests/test_gpu_spmv.py tests/test_gpu_iter.py -x -q 2>&1 | tail -8
+export VARIANTS='[{"num_tiles":0,"workload_size":1024},{"num_tiles":0,"workload_size":512},{"tile_width":49152,"num_tiles":1,"workload_size":1024},{"tile_width":24576,"num_tiles":3,"workload_size":1024},{"tile_width":24576,"num_tiles":8,"workload_size":1024},{"tile_width":24576,"num_tiles":16,"workload_size":1024}]'
+python bench/explore_spmv.py c2 2>&1 | tail -7
+python bench/explore_spmv.py c2 --pattern 2>&1 | tail -7

@@ -91,6 +91,8 @@ typedef struct {
     int32_t tile_staged[64];
     double tile_predicted_us[64];
     int32_t composite_threshold[64]; /* first row length stored column major in each tile */
+    int32_t resident_warps;     /* warps of one persistent tile launch (MAX_ACT_WARP of Eq. 1) */
+    int32_t perf_table_loaded;  /* 1: measured offline table (Sec. 3.3), 0: built-in estimate */
 } spmv_plan_stats_t;
 
 /* Host view of the layout arrays (Format v1), valid while the plan lives, when the
@@ -147,7 +149,7 @@ typedef struct {
     double c;              /* PageRank damping (0.85, L430) / RWR c (0.9, L456); unused by HITS */
     double tol;            /* L1 stopping threshold on the change (reading R2); default 1e-6 */
     int32_t max_iter;      /* default 1000 */
-    int32_t hits_norm;     /* 2 = unit L2 halves (default), 1 = halves sum to 1 (paper, L440) */
+    int32_t hits_norm;     /* 1 = halves sum to 1 (paper, L440; default), 2 = unit L2 halves */
     int32_t fixed_iters;   /* > 0: run exactly this many iterations (parity at equal k) */
 } spmv_iter_opts;
 void spmv_iter_opts_default(spmv_iter_opts* o, int algo);
@@ -164,7 +166,10 @@ typedef struct {
 /* Graph input for all three: adjacency A of G = (V,E), CSR with row u listing the targets v of
  * u -> v (A(u,v) = 1, L414); duplicates collapse, self loops are kept.
  * A solver builds its plan once (preprocessing amortised over iterations, L98) and can run many
- * times; `comm` = NULL runs on one GPU, else the row-partitioned multi-GPU path (Sec. 3.2). */
+ * times; `comm` = NULL runs on one GPU, else the row-partitioned multi-GPU path (Sec. 3.2):
+ * every rank passes the whole graph, owns the rows bitonic_partition gives it, runs its local
+ * tiled-composite SpMV with the fused epilogue, and the next x plus the fp64 partials are
+ * exchanged by one NCCL allgather per iteration (PageRank and RWR; HITS returns SPMV_EINVAL). */
 spmv_status spmv_solver_create(int algo, int64_t n, int64_t m, const int64_t* row_ptr,
                                const int32_t* col, const spmv_iter_opts* it,
                                const spmv_options* opt, spmv_comm comm, int device,
@@ -193,6 +198,13 @@ spmv_status rwr(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* col
 /* Bitonic (snake) partition of rows by length over P ranks (L108, reading R25):
  * owner_out[i] in [0,P).  Row counts differ by at most 1.  Errors: EINVAL, ERANGE (P > rows). */
 spmv_status bitonic_partition(int64_t n_rows, const int64_t* row_len, int32_t P, int32_t* owner_out);
+
+/* Ownership and slot layout of the row-partitioned path: owner_out[i] = bitonic owner of row i,
+ * local_index_out[i] = its position among its owner's rows (ascending row id), *slot_rows = the
+ * largest per-rank row count (every rank's allgather slot holds that many values).
+ * Errors as bitonic_partition. */
+spmv_status spmv_partition_plan(int64_t n_rows, const int64_t* row_len, int32_t P, int32_t* owner_out,
+                                int64_t* local_index_out, int64_t* slot_rows);
 
 /* Communicator over NCCL (loaded at run time).  nccl_unique_id: the 128-byte ncclUniqueId,
  * created by rank 0 with spmv_comm_unique_id() and broadcast by the caller (e.g. over a torch

@@ -2,8 +2,8 @@
 iterations on it (Yang, Parthasarathy & Sadayappan, VLDB 2011).  The compute path is the C-ABI
 library lib/libtcspmv.so (include/spmv.h); this package only marshals arguments."""
 from .api import (Comm, Plan, Solver, bitonic_partition, hits, iter_opts, make_options, pagerank,
-                  rwr)
+                  partition_plan, rwr)
 from ._capi import LIB_PATH, SpmvError, lib
 
-__all__ = ["Plan", "Solver", "Comm", "pagerank", "hits", "rwr", "bitonic_partition",
+__all__ = ["Plan", "Solver", "Comm", "pagerank", "hits", "rwr", "bitonic_partition", "partition_plan",
            "make_options", "iter_opts", "SpmvError", "lib", "LIB_PATH"]

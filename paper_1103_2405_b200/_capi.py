@@ -6,7 +6,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtcspmv.so")
+LIB_PATH = os.environ.get("TCSPMV_LIB") or os.path.join(_HERE, "lib", "libtcspmv.so")
 
 c_i32, c_i64, c_u8, c_u32, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8,
                                                  ctypes.c_uint32, ctypes.c_float, ctypes.c_double,
@@ -32,7 +32,8 @@ class PlanStats(ctypes.Structure):
                 ("wl", c_i32 * 64), ("tile_nnz", c_i64 * 64), ("tile_rows", c_i64 * 64),
                 ("tile_col_lo", c_i64 * 64), ("tile_col_hi", c_i64 * 64),
                 ("tile_staged", c_i32 * 64), ("tile_predicted_us", c_f64 * 64),
-                ("composite_threshold", c_i32 * 64)]
+                ("composite_threshold", c_i32 * 64), ("resident_warps", c_i32),
+                ("perf_table_loaded", c_i32)]
 
 
 class LayoutView(ctypes.Structure):
@@ -86,6 +87,7 @@ SIGNATURES = {
     "rwr": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i64, ctypes.POINTER(IterOpts), ctypes.POINTER(Options),
                     c_vp, ctypes.c_int, c_vp, ctypes.POINTER(IterResult)]),
     "bitonic_partition": (c_i32, [c_i64, c_vp, c_i32, c_vp]),
+    "spmv_partition_plan": (c_i32, [c_i64, c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(c_i64)]),
     "spmv_comm_unique_id": (c_i32, [c_vp]),
     "spmv_comm_create": (c_i32, [ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     "spmv_comm_destroy": (None, [c_vp]),

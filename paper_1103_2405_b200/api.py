@@ -72,7 +72,8 @@ def _stats_dict(s: C.PlanStats) -> dict:
                 tile_col_lo=list(s.tile_col_lo[:T]), tile_col_hi=list(s.tile_col_hi[:T]),
                 tile_staged=list(s.tile_staged[:T]),
                 tile_predicted_us=list(s.tile_predicted_us[:T]),
-                composite_threshold=list(s.composite_threshold[:T]))
+                composite_threshold=list(s.composite_threshold[:T]),
+                resident_warps=s.resident_warps, perf_table_loaded=bool(s.perf_table_loaded))
 
 
 class Plan:
@@ -254,6 +255,17 @@ def bitonic_partition(row_len, P: int) -> np.ndarray:
     return owner[: len(rl)]
 
 
+def partition_plan(row_len, P: int):
+    """(owner, local_index, slot_rows) of the row-partitioned path (spmv_partition_plan)."""
+    rl = _np(row_len, np.int64)
+    owner = np.zeros(max(len(rl), 1), np.int32)
+    lidx = np.zeros(max(len(rl), 1), np.int64)
+    S = ctypes.c_int64(0)
+    check(C.lib().spmv_partition_plan(len(rl), _ptr(rl), int(P), owner.ctypes.data, lidx.ctypes.data,
+                                      ctypes.byref(S)), "spmv_partition_plan")
+    return owner[: len(rl)], lidx[: len(rl)], int(S.value)
+
+
 class Comm:
     """NCCL communicator for the row-partitioned path (Sec. 3.2).  The 128-byte unique id is
     created on rank 0 and broadcast by the caller (e.g. over a torch process group)."""
@@ -263,6 +275,17 @@ class Comm:
         buf = ctypes.create_string_buffer(128)
         check(C.lib().spmv_comm_unique_id(buf), "spmv_comm_unique_id")
         return buf.raw
+
+    @classmethod
+    def from_torch(cls, device: int, group=None):
+        """Bootstrap over an initialised torch.distributed process group: rank 0 draws the NCCL
+        unique id, every rank receives it by broadcast."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if (rank == 0 and world > 1) else b"\0" * 128]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(rank, world, obj[0], device)
 
     def __init__(self, rank: int, world: int, uid: bytes, device: int):
         buf = ctypes.create_string_buffer(bytes(uid), 128)

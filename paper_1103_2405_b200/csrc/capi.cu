@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -55,6 +56,15 @@ static void free_device(spmv_plan_s* p) {
     cudaSetDevice(cur);
 }
 
+// Streaming kernel buffers: the largest workload of the plan sets the per-warp buffer size.
+static cudaError_t build_stream_tables(spmv_plan_s* p) {
+    int64_t maxspan = 0;
+    for (const auto& d : p->L.desc) maxspan = std::max<int64_t>(maxspan, (int64_t)d.h * d.w);
+    p->stage_slots = (int32_t)std::max<int64_t>(64, (maxspan + 3) / 4 * 4);
+    p->stream_grid = p->sm_count;
+    return cudaSuccess;
+}
+
 // build the plan (host) and upload it; shared by spmv_plan_create and the solvers
 spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col, const float* val, const spmv_options* opt_in,
@@ -79,11 +89,12 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     if (st) return st;
     BuildParams bp;
     std::vector<double> pred;
-    st = choose_params(P, opt, sm_count, bp, pred);
+    int32_t table_loaded = 0;
+    st = choose_params(P, opt, sm_count, bp, pred, &table_loaded);
     if (st) return st;
     spmv_plan_s* p = new spmv_plan_s();
     p->n_rows = n_rows; p->n_cols = n_cols; p->nnz = nnz; p->pattern = opt.pattern != 0;
-    p->device = device; p->opt = opt; p->sm_count = sm_count;
+    p->device = device; p->opt = opt; p->sm_count = sm_count; p->perf_table_loaded = table_loaded;
     p->opt.workload_sizes = nullptr; p->opt.perf_table_path = nullptr;
     st = pack_layout(P, bp, p->L);
     if (st) { delete p; return st; }
@@ -98,7 +109,8 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     p->n_chunks = p->L.n_chunks;
     predict_plan(*p, pred);
     for (int32_t t = 0; t < p->num_tiles; ++t)
-        p->tiles[t].staged = (opt.stage_x != 0) && (p->tiles[t].col_hi - p->tiles[t].col_lo) * 4 <= 227 * 1024;
+        p->tiles[t].staged = (opt.stage_x != 0) && (p->tiles[t].col_hi - p->tiles[t].col_lo) * 4 <= 227 * 1024 &&
+                             (p->tiles[t].col_lo % 4 == 0);
     if (device >= 0) {
         cudaError_t e;
         int64_t& b = p->device_bytes;
@@ -116,6 +128,11 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
         if ((e = upload(&p->d_partials, zf, b)) || (e = upload(&p->d_counters, zi, b)) ||
             (e = upload(&p->d_xp, xpz, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
+        }
+        const char* kenv = std::getenv("TCSPMV_KERNEL");
+        p->stream = !(kenv && std::string(kenv) == "classic");
+        if (p->stream && (e = build_stream_tables(p))) {
+            free_device(p); delete p; return cuda_status(e, "stage tables");
         }
         if ((e = setup_grids<EpiStore>(*p, p->grid_tile))) {
             free_device(p); delete p; return cuda_status(e, "occupancy");
@@ -281,6 +298,8 @@ spmv_status spmv_plan_stats(spmv_plan p, spmv_plan_stats_t* o) {
         o->tile_col_lo[t] = ti.col_lo; o->tile_col_hi[t] = ti.col_hi; o->tile_staged[t] = ti.staged;
         o->tile_predicted_us[t] = ti.pred_us; o->composite_threshold[t] = ti.threshold;
     }
+    o->resident_warps = p->grid_tile.empty() ? 0 : p->grid_tile.back() * (p->stream ? kStreamThreads / 32 : kWarps);
+    o->perf_table_loaded = p->perf_table_loaded;
     return SPMV_OK;
 }
 

@@ -8,6 +8,9 @@
 #include <numeric>
 #include <vector>
 
+#include "epilogues.cuh"
+#include "graph_build.h"
+#include "launch.cuh"
 #include "solver.h"
 
 using namespace tc;
@@ -74,6 +77,21 @@ spmv_status bitonic_partition(int64_t n_rows, const int64_t* row_len, int32_t P,
     return SPMV_OK;
 }
 
+// Row ownership and slot layout of the row-partitioned path (Sec. 3.2): owner by bitonic
+// partition; inside a rank its rows keep ascending id order (local_index); every rank's slot
+// holds slot_rows entries (the largest rank count, so the allgather has equal counts).
+__attribute__((visibility("default")))
+spmv_status spmv_partition_plan(int64_t n_rows, const int64_t* row_len, int32_t P, int32_t* owner,
+                                int64_t* local_index, int64_t* slot_rows) {
+    spmv_status s = bitonic_partition(n_rows, row_len, P, owner);
+    if (s) return s;
+    if (!local_index || !slot_rows) { set_error("null argument"); return SPMV_EINVAL; }
+    std::vector<int64_t> cnt(P, 0);
+    for (int64_t i = 0; i < n_rows; ++i) local_index[i] = cnt[owner[i]]++;
+    *slot_rows = n_rows ? *std::max_element(cnt.begin(), cnt.end()) : 0;
+    return SPMV_OK;
+}
+
 __attribute__((visibility("default"))) spmv_status spmv_comm_unique_id(void* id_out) {
     if (!id_out) { set_error("null argument"); return SPMV_EINVAL; }
     if (!g_nccl.load()) { set_error("libnccl.so.2 not found"); return SPMV_ENCCL; }
@@ -109,18 +127,260 @@ __attribute__((visibility("default"))) void spmv_comm_destroy(spmv_comm c) {
 
 }  // extern "C"
 
-spmv_status solver_create_dist(int, int64_t, int64_t, const int64_t*, const int32_t*,
-                               const spmv_iter_opts*, const spmv_options*, spmv_comm, int,
-                               spmv_solver*) {
-    set_error("multi-GPU solver: not built in this version");
-    return SPMV_EINVAL;
+
+// ------------------------------------------------------------------ row-partitioned solvers
+namespace {
+
+struct Dist {
+    int P = 1, rank = 0;
+    int64_t n_local = 0, S = 0, slot = 0;    // owned rows, slot rows, slot floats (S + partials)
+    int64_t nzc = 0;                         // local columns with entries (plan column prefix)
+    std::vector<int64_t> gpos;               // vertex -> position in the gathered buffer
+    std::vector<int32_t> owned;              // local row -> vertex
+    int64_t q_local = -1;
+    float* d_G = nullptr;                    // gathered buffer: P slots
+    int32_t* d_idx = nullptr;                // x'[k] = G[idx[k]] for k < nzc
+};
+
+constexpr int64_t kPartialFloats = 8;        // two fp64 partials (+ padding), 16-byte multiple
+
+__global__ void dist_permute(const float* __restrict__ G, const int32_t* __restrict__ idx,
+                             float* __restrict__ xp, int64_t nzc, const tc::Ctrl* ctrl) {
+    if (*(volatile const int32_t*)&ctrl->done) return;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nzc; k += (int64_t)gridDim.x * blockDim.x)
+        xp[k] = __ldg(G + __ldg(idx + k));
 }
-spmv_status solver_run_dist(spmv_solver, int64_t, void*, spmv_iter_result*) {
-    set_error("multi-GPU solver: not built in this version");
-    return SPMV_EINVAL;
+
+// sum the P ranks' partials in rank order (identical on every rank: deterministic), advance
+__global__ void dist_finalize(const float* G, int64_t slot, int64_t S, int P, tc::Ctrl* ctrl, int rwr) {
+    if (threadIdx.x != 0 || *(volatile int32_t*)&ctrl->done) return;
+    double res = 0.0, dm = 0.0;
+    for (int r = 0; r < P; ++r) {
+        const double* part = reinterpret_cast<const double*>(G + (int64_t)r * slot + S);
+        res += part[0];
+        dm += part[1];
+    }
+    if (!rwr) ctrl->tele = ctrl->c * dm * ctrl->inv_n + (1.0 - ctrl->c) * ctrl->inv_n;
+    ctrl->dmass = dm;
+    ctrl->residual = res;
+    ctrl->iter += 1;
+    bool done = ctrl->fixed_iters > 0 ? ctrl->iter >= ctrl->fixed_iters : (res < ctrl->tol || ctrl->iter >= ctrl->max_iter);
+    ctrl->done = done ? 1 : 0;
 }
-spmv_status solver_result_dist(spmv_solver, float*, float*) {
-    set_error("multi-GPU solver: not built in this version");
-    return SPMV_EINVAL;
+
+__global__ void dist_init(float* p, float* zslot, const float* inv, int64_t n_local, int rwr,
+                          int64_t q_local, float p0) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += (int64_t)gridDim.x * blockDim.x) {
+        float v = rwr ? (i == q_local ? 1.0f : 0.0f) : p0;
+        p[i] = v;
+        zslot[i] = v * inv[i];
+    }
 }
-void solver_destroy_dist(spmv_solver) {}
+
+__global__ void copy_f(const float* a, float* b, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
+    if (c->world == 1) return SPMV_OK;
+    return nccl_status(g_nccl.AllGather(G + (int64_t)c->rank * slot, G, (size_t)slot, ncclFloat32, c->comm, st),
+                       "ncclAllGather");
+}
+
+}  // namespace
+
+
+spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* row_ptr,
+                               const int32_t* col, const spmv_iter_opts* it,
+                               const spmv_options* opt_in, spmv_comm comm, int device,
+                               spmv_solver* out) {
+    (void)m;
+    if (algo == SPMV_ALGO_HITS) { set_error("row-partitioned HITS is not built in this version"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    spmv_solver_s* s = new spmv_solver_s();
+    Dist* D = new Dist();
+    s->algo = algo; s->n = n; s->N = n; s->device = device; s->comm = comm; s->dist = D;
+    if (it) s->it = *it; else spmv_iter_opts_default(&s->it, algo);
+    D->P = comm->world; D->rank = comm->rank;
+    spmv_status st = SPMV_OK;
+    try {
+        std::vector<int64_t> arp; std::vector<int32_t> acol;
+        clean_adjacency(n, row_ptr, col, arp, acol);
+        std::vector<int64_t> mrp, len; std::vector<int32_t> mcol;
+        build_iteration_matrix(algo, n, arp, acol, mrp, mcol, len);
+        // partition rows of M (bitonic over row lengths, Sec. 3.2)
+        std::vector<int64_t> rl(n);
+        for (int64_t i = 0; i < n; ++i) rl[i] = mrp[i + 1] - mrp[i];
+        std::vector<int32_t> owner(n);
+        std::vector<int64_t> lidx(n);
+        int64_t S = 0;
+        if ((st = spmv_partition_plan(n, rl.data(), D->P, owner.data(), lidx.data(), &S))) throw st;
+        D->S = (S + 3) / 4 * 4;
+        D->slot = D->S + kPartialFloats;
+        D->gpos.resize(n);
+        for (int64_t i = 0; i < n; ++i) {
+            D->gpos[i] = (int64_t)owner[i] * D->slot + lidx[i];
+            if (owner[i] == D->rank) D->owned.push_back((int32_t)i);
+        }
+        D->n_local = (int64_t)D->owned.size();
+        // local rows (ascending vertex id = local index order), original column ids
+        std::vector<int64_t> lrp(D->n_local + 1, 0);
+        for (int64_t r = 0; r < D->n_local; ++r) lrp[r + 1] = lrp[r] + rl[D->owned[r]];
+        std::vector<int32_t> lcol(lrp[D->n_local]);
+        std::vector<char> seen(n, 0);
+        for (int64_t r = 0; r < D->n_local; ++r) {
+            const int64_t v = D->owned[r];
+            std::copy(mcol.begin() + mrp[v], mcol.begin() + mrp[v + 1], lcol.begin() + lrp[r]);
+            for (int64_t k = mrp[v]; k < mrp[v + 1]; ++k) seen[mcol[k]] = 1;
+        }
+        for (int64_t j = 0; j < n; ++j) D->nzc += seen[j];
+        spmv_options opt;
+        if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
+        opt.pattern = 1;
+        if ((st = tc::create_plan(D->n_local, n, lrp[D->n_local], lrp.data(), lcol.data(), nullptr, &opt, device, &s->plan))) throw st;
+        spmv_plan_s* p = s->plan;
+        // the plan's columns are ordered by local length: the first nzc have entries
+        std::vector<int32_t> idx(D->nzc);
+        for (int64_t k = 0; k < D->nzc; ++k) idx[k] = (int32_t)D->gpos[p->perm[k]];
+        std::vector<float> inv(std::max<int64_t>(D->n_local, 1), 0.0f);
+        int64_t n_dangling = 0;
+        for (int64_t u = 0; u < n; ++u) n_dangling += (len[u] == 0);
+        for (int64_t r = 0; r < D->n_local; ++r) {
+            const int64_t v = D->owned[r];
+            inv[r] = len[v] ? (float)(1.0 / (double)len[v]) : 0.0f;
+        }
+        s->n_dangling = n_dangling;
+#define CKD(x) do { if ((e = (x)) != cudaSuccess) { st = cuda_status(e, #x); throw st; } } while (0)
+        CKD(cudaMalloc(&D->d_G, (size_t)D->P * D->slot * sizeof(float)));
+        CKD(cudaMemset(D->d_G, 0, (size_t)D->P * D->slot * sizeof(float)));
+        CKD(cudaMalloc(&D->d_idx, std::max<int64_t>(D->nzc, 1) * sizeof(int32_t)));
+        if (D->nzc) CKD(cudaMemcpy(D->d_idx, idx.data(), D->nzc * sizeof(int32_t), cudaMemcpyHostToDevice));
+        const int64_t nl = std::max<int64_t>(D->n_local, 1);
+        CKD(cudaMalloc(&s->d_p, (nl + 4) * sizeof(float)));
+        CKD(cudaMalloc(&s->d_y, (nl + 4) * sizeof(float)));
+        CKD(cudaMalloc(&s->d_inv, nl * sizeof(float)));
+        CKD(cudaMemcpy(s->d_inv, inv.data(), nl * sizeof(float), cudaMemcpyHostToDevice));
+        CKD(cudaMalloc(&s->d_ctrl, sizeof(Ctrl)));
+        CKD(cudaMemset(s->d_ctrl, 0, sizeof(Ctrl)));
+        CKD(setup_grids<EpiAffine>(*p, s->grids));
+        int32_t slots = 0;
+        for (int32_t t = 0; t <= p->num_tiles; ++t) {
+            if (p->tiles[t].wl_end == p->tiles[t].wl_begin) continue;
+            s->tiles_used.push_back(t);
+            s->slot_base.push_back(slots);
+            slots += s->grids[t];
+        }
+        s->total_slots = slots;
+        CKD(cudaMalloc(&s->d_slots, (size_t)std::max(slots, 1) * 2 * sizeof(double)));
+#undef CKD
+    } catch (spmv_status code) {
+        st = code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed"); st = SPMV_ENOMEM;
+    }
+    if (st) { solver_destroy_dist(s); return st; }
+    *out = s;
+    return SPMV_OK;
+}
+
+spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res) {
+    Dist* D = static_cast<Dist*>(s->dist);
+    spmv_plan_s* p = s->plan;
+    if (s->algo == SPMV_ALGO_RWR && (query < 0 || query >= s->n)) { set_error("query out of range"); return SPMV_ERANGE; }
+    cudaError_t e = cudaSetDevice(s->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!st) {
+        if (!s->own_stream && (e = cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking)))
+            return cuda_status(e, "stream");
+        st = s->own_stream;
+    }
+    const int rwr = s->algo == SPMV_ALGO_RWR;
+    D->q_local = -1;
+    if (rwr && (int32_t)(D->gpos[query] / D->slot) == D->rank) D->q_local = D->gpos[query] % D->slot;
+    Ctrl c{};
+    const double n = (double)s->n;
+    c.c = s->it.c; c.tol = s->it.tol; c.max_iter = s->it.max_iter; c.fixed_iters = s->it.fixed_iters;
+    c.inv_n = 1.0 / n; c.residual = INFINITY; c.q = (int32_t)D->q_local;
+    c.tele = rwr ? 0.0 : c.c * ((double)s->n_dangling / n) / n + (1.0 - c.c) / n;
+    if ((e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st))) return cuda_status(e, "ctrl");
+    float* zslot = D->d_G + (int64_t)D->rank * D->slot;
+    const int g = p->sm_count * 4;
+    dist_init<<<g, 256, 0, st>>>(s->d_p, zslot, s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
+    spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
+    if (ss) return ss;
+    dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    Ctrl* hc = nullptr;
+    cudaMallocHost(&hc, sizeof(Ctrl));
+    const int batch = 8;
+    int launched = 0;
+    while (true) {
+        for (int b = 0; b < batch; ++b) {
+            const size_t nu = s->tiles_used.size();
+            for (size_t i = 0; i < nu; ++i) {
+                EpiAffine epi{};
+                epi.y = s->d_y; epi.p = s->d_p; epi.z_next = zslot; epi.inv_deg = s->d_inv;
+                epi.ctrl = s->d_ctrl; epi.slots = s->d_slots; epi.slot_base = s->slot_base[i];
+                epi.total_slots = s->total_slots; epi.is_last = (i + 1 == nu); epi.cond = 0;
+                epi.rwr = rwr;
+                epi.dist_out = reinterpret_cast<double*>(zslot + D->S);
+                if ((e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], p->d_xp, epi, st)))
+                    return cuda_status(e, "tile launch");
+            }
+            if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
+            if ((ss = allgather(s->comm, D->d_G, D->slot, st))) return ss;
+            dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->slot, D->S, D->P, s->d_ctrl, rwr);
+            dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+            ++launched;
+        }
+        cudaMemcpyAsync(hc, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+        if ((e = cudaStreamSynchronize(st))) { cudaFreeHost(hc); return cuda_status(e, "iteration loop"); }
+        if (hc->done || launched > s->it.max_iter + batch) break;
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    c = *hc;
+    cudaFreeHost(hc);
+    s->last = c;
+    if (res) {
+        res->iterations = c.iter; res->residual = c.residual;
+        res->converged = s->it.fixed_iters > 0 ? 1 : (c.residual < s->it.tol);
+        res->ms_total = ms; res->us_per_iter = c.iter ? 1000.0 * ms / c.iter : 0.0;
+        res->predicted_us_per_iter = p->predicted_us;
+    }
+    if (s->it.fixed_iters <= 0 && !(c.residual < s->it.tol)) { set_error("max_iter reached"); return SPMV_ENOCONV; }
+    return SPMV_OK;
+}
+
+spmv_status solver_result_dist(spmv_solver s, float* out0, float*) {
+    Dist* D = static_cast<Dist*>(s->dist);
+    cudaSetDevice(s->device);
+    cudaStream_t st = s->own_stream;
+    float* slot = D->d_G + (int64_t)D->rank * D->slot;
+    copy_f<<<s->plan->sm_count * 4, 256, 0, st>>>(s->d_p, slot, D->n_local);
+    spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
+    if (ss) return ss;
+    std::vector<float> G((size_t)D->P * D->slot);
+    cudaError_t e = cudaMemcpyAsync(G.data(), D->d_G, G.size() * sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    if (e) return cuda_status(e, "result");
+    for (int64_t u = 0; u < s->n; ++u) out0[u] = G[D->gpos[u]];
+    return SPMV_OK;
+}
+
+void solver_destroy_dist(spmv_solver s) {
+    Dist* D = static_cast<Dist*>(s->dist);
+    cudaSetDevice(s->device);
+    if (D) { cudaFree(D->d_G); cudaFree(D->d_idx); delete D; }
+    if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    cudaFree(s->d_p); cudaFree(s->d_y); cudaFree(s->d_inv); cudaFree(s->d_ctrl); cudaFree(s->d_slots);
+    if (s->plan) spmv_plan_destroy(s->plan);
+    delete s;
+}

@@ -23,6 +23,8 @@
 #include <cstring>
 #include <vector>
 
+#include "epilogues.cuh"
+#include "graph_build.h"
 #include "launch.cuh"
 #include "solver.h"
 
@@ -31,261 +33,6 @@ namespace tc {
 spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col, const float* val, const spmv_options* opt_in,
                         int device, spmv_plan_s** out);
-
-// ------------------------------------------------------------------ device helpers
-template <int NP>
-__device__ __forceinline__ void block_reduce_to_slot(double (&v)[NP], double* slot) {
-    __shared__ double red[kWarps][NP];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    #pragma unroll
-    for (int k = 0; k < NP; ++k)
-        for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-    if (lane == 0) {
-        #pragma unroll
-        for (int k = 0; k < NP; ++k) red[warp][k] = v[k];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        #pragma unroll
-        for (int k = 0; k < NP; ++k) {
-            double s = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][k];
-            slot[k] = s;
-        }
-    }
-}
-
-// true in exactly one (the last arriving) block of this launch
-__device__ __forceinline__ bool last_block(uint32_t* ticket) {
-    __shared__ bool am_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        uint32_t t = atomicAdd(ticket, 1u);
-        am_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (am_last) __threadfence();
-    return am_last;
-}
-
-// fixed-order sum of slots[0..n)[k] by the whole block; result valid in thread 0
-template <int NP>
-__device__ __forceinline__ void block_sum_slots(const double* slots, int n, double (&out)[NP]) {
-    double v[NP];
-    #pragma unroll
-    for (int k = 0; k < NP; ++k) v[k] = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        #pragma unroll
-        for (int k = 0; k < NP; ++k) v[k] += __ldcg(slots + (size_t)i * NP + k);
-    }
-    __shared__ double tmp[NP];
-    block_reduce_to_slot<NP>(v, tmp);
-    __syncthreads();
-    #pragma unroll
-    for (int k = 0; k < NP; ++k) out[k] = tmp[k];
-}
-
-__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, bool more) {
-    if (h) cudaGraphSetConditional(h, more ? 1u : 0u);
-}
-
-__device__ __forceinline__ bool iteration_done(Ctrl* c, double res) {
-    c->residual = res;
-    c->iter += 1;
-    bool done;
-    if (c->fixed_iters > 0) done = c->iter >= c->fixed_iters;
-    else done = (res < c->tol) || (c->iter >= c->max_iter);
-    c->done = done ? 1 : 0;
-    return done;
-}
-
-// ------------------------------------------------------------------ PageRank / RWR epilogue
-struct EpiAffine {
-    float* y; float* p; float* z_next; const float* inv_deg;
-    Ctrl* ctrl; double* slots; int32_t slot_base, total_slots, is_last;
-    cudaGraphConditionalHandle cond;
-    int32_t rwr;
-    // per thread
-    float c, tele; int32_t q; double res, dm;
-
-    __device__ __forceinline__ bool begin() {
-        if (*(volatile int32_t*)&ctrl->done) return false;
-        c = (float)ctrl->c; tele = (float)ctrl->tele; q = ctrl->q;
-        res = 0.0; dm = 0.0;
-        return true;
-    }
-    __device__ __forceinline__ void write(uint32_t ent, float v) {
-        const uint32_t r = ent & ROW_MASK;
-        if (ent & FLAG_ACC) v += y[r];
-        if (!(ent & FLAG_FINAL)) { y[r] = v; return; }
-        float pn = fmaf(c, v, tele);
-        if (rwr && (int32_t)r == q) pn += 1.0f - c;
-        const float po = p[r];
-        res += fabs((double)pn - (double)po);
-        p[r] = pn;
-        const float id = __ldg(inv_deg + r);
-        z_next[r] = pn * id;
-        if (id == 0.0f) dm += (double)pn;
-    }
-    __device__ __forceinline__ void end() {
-        double v[2] = {res, dm};
-        block_reduce_to_slot<2>(v, slots + 2 * (size_t)(slot_base + blockIdx.x));
-        if (!is_last) return;
-        if (!last_block(&ctrl->ticket)) return;
-        double s[2];
-        block_sum_slots<2>(slots, total_slots, s);
-        if (threadIdx.x == 0) {
-            ctrl->ticket = 0;
-            // next iteration's additive term: PageRank c*D/n + (1-c)/n (reading R1); RWR 0
-            if (!rwr) ctrl->tele = ctrl->c * s[1] * ctrl->inv_n + (1.0 - ctrl->c) * ctrl->inv_n;
-            ctrl->dmass = s[1];
-            bool done = iteration_done(ctrl, s[0]);
-            __threadfence();
-            set_cond(cond, !done);
-        }
-    }
-};
-
-// ------------------------------------------------------------------ HITS epilogues
-struct EpiHitsSpmv {
-    float* y; const uint8_t* half;
-    Ctrl* ctrl; double* slots; int32_t slot_base, total_slots, is_last, l2;
-    double s0, s1;
-    __device__ __forceinline__ bool begin() {
-        if (*(volatile int32_t*)&ctrl->done) return false;
-        s0 = 0.0; s1 = 0.0;
-        return true;
-    }
-    __device__ __forceinline__ void write(uint32_t ent, float v) {
-        const uint32_t r = ent & ROW_MASK;
-        if (ent & FLAG_ACC) v += y[r];
-        y[r] = v;
-        if (!(ent & FLAG_FINAL)) return;
-        const double d = l2 ? (double)v * (double)v : fabs((double)v);
-        if (__ldg(half + r)) s1 += d; else s0 += d;
-    }
-    __device__ __forceinline__ void end() {
-        double v[2] = {s0, s1};
-        block_reduce_to_slot<2>(v, slots + 2 * (size_t)(slot_base + blockIdx.x));
-        if (!is_last) return;
-        if (!last_block(&ctrl->ticket)) return;
-        double s[2];
-        block_sum_slots<2>(slots, total_slots, s);
-        if (threadIdx.x == 0) {
-            ctrl->ticket = 0;
-            ctrl->norm[0] = l2 ? sqrt(s[0]) : s[0];
-            ctrl->norm[1] = l2 ? sqrt(s[1]) : s[1];
-        }
-    }
-};
-
-// a' = y_a / |y_a|, h' = y_h / |y_h| (zero half -> uniform, reading R5); L1 change accumulated
-__global__ void __launch_bounds__(kThreads) hits_normalize(const float* __restrict__ y,
-                                                           float* __restrict__ v,
-                                                           const uint8_t* __restrict__ half,
-                                                           int64_t N, Ctrl* ctrl, double* slots,
-                                                           cudaGraphConditionalHandle cond) {
-    if (*(volatile int32_t*)&ctrl->done) return;
-    const double n0 = ctrl->norm[0], n1 = ctrl->norm[1];
-    const float uni = (float)ctrl->uniform;
-    const float s0 = n0 > 0.0 ? (float)(1.0 / n0) : 0.0f, s1 = n1 > 0.0 ? (float)(1.0 / n1) : 0.0f;
-    double res = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < N; i += (int64_t)gridDim.x * kThreads) {
-        const int h = half[i];
-        const double nn = h ? n1 : n0;
-        const float vn = nn > 0.0 ? y[i] * (h ? s1 : s0) : uni;
-        res += fabs((double)vn - (double)v[i]);
-        v[i] = vn;
-    }
-    double acc[1] = {res};
-    block_reduce_to_slot<1>(acc, slots + blockIdx.x);
-    if (!last_block(&ctrl->ticket)) return;
-    double s[1];
-    block_sum_slots<1>(slots, gridDim.x, s);
-    if (threadIdx.x == 0) {
-        ctrl->ticket = 0;
-        bool done = iteration_done(ctrl, s[0]);
-        __threadfence();
-        set_cond(cond, !done);
-    }
-}
-
-__global__ void init_affine(float* p, float* z, const float* inv_deg, int64_t n, int32_t rwr,
-                            int32_t q, float p0) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float v = rwr ? (i == q ? 1.0f : 0.0f) : p0;
-        p[i] = v;
-        z[i] = v * inv_deg[i];
-    }
-}
-__global__ void init_fill(float* v, int64_t n, float val) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        v[i] = val;
-}
-
-// ------------------------------------------------------------------ host: graph matrices
-// counting sort permutation of [0,N) by (len desc, id asc): pi[id] = new position
-static void order_by_length(const std::vector<int64_t>& len, std::vector<int32_t>& pi) {
-    const int64_t N = (int64_t)len.size();
-    int64_t mx = 0;
-    for (auto l : len) mx = std::max(mx, l);
-    std::vector<int64_t> start(mx + 2, 0);
-    for (auto l : len) start[mx - l + 1]++;
-    for (int64_t b = 0; b <= mx; ++b) start[b + 1] += start[b];
-    pi.assign(N, 0);
-    for (int64_t i = 0; i < N; ++i) pi[i] = (int32_t)start[mx - len[i]]++;
-}
-
-// dedupe each row of an adjacency CSR (sorted unique targets per row)
-static void clean_adjacency(int64_t n, const int64_t* rp, const int32_t* col,
-                            std::vector<int64_t>& orp, std::vector<int32_t>& ocol) {
-    std::vector<int64_t> len(n);
-    ocol.assign(col, col + rp[n]);
-    #pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t u = 0; u < n; ++u) {
-        int32_t* b = ocol.data() + rp[u];
-        int32_t* e = ocol.data() + rp[u + 1];
-        std::sort(b, e);
-        len[u] = std::unique(b, e) - b;
-    }
-    orp.assign(n + 1, 0);
-    for (int64_t u = 0; u < n; ++u) orp[u + 1] = orp[u] + len[u];
-    std::vector<int32_t> packed(orp[n]);
-    #pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t u = 0; u < n; ++u)
-        std::copy(ocol.begin() + rp[u], ocol.begin() + rp[u] + len[u], packed.begin() + orp[u]);
-    ocol.swap(packed);
-}
-
-// relabelled CSR of a matrix given as a list of (row, col) by a generator callback over rows
-struct Coo { std::vector<int64_t> rp; std::vector<int32_t> col; };
-
-// rows of the relabelled matrix: entries of original row r go to row pi[r], cols mapped by pi
-static void relabel_csr(int64_t N, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
-                        const std::vector<int32_t>& pi, Coo& out) {
-    out.rp.assign(N + 1, 0);
-    for (int64_t r = 0; r < N; ++r) out.rp[pi[r] + 1] = rp[r + 1] - rp[r];
-    for (int64_t i = 0; i < N; ++i) out.rp[i + 1] += out.rp[i];
-    out.col.resize(rp[N]);
-    #pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t r = 0; r < N; ++r) {
-        int64_t d = out.rp[pi[r]];
-        for (int64_t k = rp[r]; k < rp[r + 1]; ++k) out.col[d++] = pi[col[k]];
-    }
-}
-
-// transpose of an n x n pattern CSR (row v lists sources u ascending)
-static void transpose(int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
-                      std::vector<int64_t>& trp, std::vector<int32_t>& tcol) {
-    trp.assign(n + 1, 0);
-    for (int64_t k = 0; k < rp[n]; ++k) trp[col[k] + 1]++;
-    for (int64_t i = 0; i < n; ++i) trp[i + 1] += trp[i];
-    tcol.resize(rp[n]);
-    std::vector<int64_t> pos(trp.begin(), trp.end() - 1);
-    for (int64_t u = 0; u < n; ++u)
-        for (int64_t k = rp[u]; k < rp[u + 1]; ++k) tcol[pos[col[k]]++] = (int32_t)u;
-}
 
 }  // namespace tc
 
@@ -300,56 +47,7 @@ static spmv_status build_solver(spmv_solver_s* s, const int64_t* row_ptr, const 
     std::vector<int64_t> len;           // column length of the iteration matrix (relabel key)
     std::vector<int64_t> mrp;           // iteration matrix in original ids
     std::vector<int32_t> mcol;
-    std::vector<float> inv_deg;
-    if (s->algo == SPMV_ALGO_PAGERANK) {
-        transpose(n, arp, acol, mrp, mcol);                       // M = A^T
-        len.resize(n);
-        for (int64_t u = 0; u < n; ++u) len[u] = arp[u + 1] - arp[u];   // column u of A^T = outdeg
-        s->N = n;
-    } else if (s->algo == SPMV_ALGO_RWR) {
-        std::vector<int64_t> trp; std::vector<int32_t> tcol;
-        transpose(n, arp, acol, trp, tcol);
-        mrp.assign(n + 1, 0);
-        std::vector<std::vector<int32_t>> tmp;                    // S = binary(A u A^T)
-        std::vector<int64_t> slen(n);
-        mcol.clear();
-        std::vector<int32_t> buf;
-        mcol.reserve(2 * arp[n]);
-        for (int64_t i = 0; i < n; ++i) {
-            buf.assign(acol.begin() + arp[i], acol.begin() + arp[i + 1]);
-            buf.insert(buf.end(), tcol.begin() + trp[i], tcol.begin() + trp[i + 1]);
-            std::sort(buf.begin(), buf.end());
-            buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
-            mcol.insert(mcol.end(), buf.begin(), buf.end());
-            mrp[i + 1] = (int64_t)mcol.size();
-        }
-        len.resize(n);
-        for (int64_t u = 0; u < n; ++u) len[u] = mrp[u + 1] - mrp[u];  // symmetric: col len = deg
-        s->N = n;
-    } else {
-        // B = [[0, A^T], [A, 0]]: row v (< n) lists n+u for u->v; row n+u lists v for u->v
-        std::vector<int64_t> trp; std::vector<int32_t> tcol;
-        transpose(n, arp, acol, trp, tcol);
-        const int64_t N = 2 * n;
-        mrp.assign(N + 1, 0);
-        for (int64_t v = 0; v < n; ++v) mrp[v + 1] = trp[v + 1] - trp[v];
-        for (int64_t u = 0; u < n; ++u) mrp[n + u + 1] = arp[u + 1] - arp[u];
-        for (int64_t i = 0; i < N; ++i) mrp[i + 1] += mrp[i];
-        mcol.resize(mrp[N]);
-        #pragma omp parallel for schedule(dynamic, 1024)
-        for (int64_t v = 0; v < n; ++v) {
-            int64_t d = mrp[v];
-            for (int64_t k = trp[v]; k < trp[v + 1]; ++k) mcol[d++] = (int32_t)(n + tcol[k]);
-        }
-        #pragma omp parallel for schedule(dynamic, 1024)
-        for (int64_t u = 0; u < n; ++u) {
-            int64_t d = mrp[n + u];
-            for (int64_t k = arp[u]; k < arp[u + 1]; ++k) mcol[d++] = acol[k];
-        }
-        len.assign(N, 0);
-        for (int64_t k = 0; k < mrp[N]; ++k) len[mcol[k]]++;   // column lengths of B
-        s->N = N;
-    }
+    s->N = build_iteration_matrix(s->algo, n, arp, acol, mrp, mcol, len);
     const int64_t N = s->N;
     order_by_length(len, s->pi);
     Coo M;
@@ -376,10 +74,12 @@ static spmv_status build_solver(spmv_solver_s* s, const int64_t* row_ptr, const 
     spmv_plan_s* p = s->plan;
     cudaError_t e;
 #define CKE(x) do { if ((e = (x)) != cudaSuccess) return cuda_status(e, #x); } while (0)
-    CKE(cudaMalloc(&s->d_p, N * sizeof(float)));
+    CKE(cudaMalloc(&s->d_p, (N + 4) * sizeof(float)));
     CKE(cudaMalloc(&s->d_y, N * sizeof(float)));
-    CKE(cudaMalloc(&s->d_z[0], N * sizeof(float)));
-    CKE(cudaMalloc(&s->d_z[1], N * sizeof(float)));
+    CKE(cudaMalloc(&s->d_z[0], (N + 4) * sizeof(float)));   // +4: 16-byte bulk copies of x
+    CKE(cudaMalloc(&s->d_z[1], (N + 4) * sizeof(float)));
+    CKE(cudaMemset(s->d_z[0], 0, (N + 4) * sizeof(float)));
+    CKE(cudaMemset(s->d_z[1], 0, (N + 4) * sizeof(float)));
     CKE(cudaMalloc(&s->d_inv, N * sizeof(float)));
     CKE(cudaMemcpy(s->d_inv, invd_pi.data(), N * sizeof(float), cudaMemcpyHostToDevice));
     CKE(cudaMalloc(&s->d_half, std::max<int64_t>(N, 1)));
@@ -469,7 +169,7 @@ extern "C" {
 __attribute__((visibility("default"))) void spmv_iter_opts_default(spmv_iter_opts* o, int algo) {
     if (!o) return;
     o->c = algo == SPMV_ALGO_RWR ? 0.9 : 0.85;
-    o->tol = 1e-6; o->max_iter = 1000; o->hits_norm = 2; o->fixed_iters = 0;
+    o->tol = 1e-6; o->max_iter = 1000; o->hits_norm = 1; o->fixed_iters = 0;
 }
 
 __attribute__((visibility("default")))

@@ -20,6 +20,7 @@ struct spmv_plan_s {
     int64_t n_workloads = 0, n_slots = 0, n_row_entries = 0, n_split = 0, n_chunks = 0;
     std::vector<tc::TileInfo> tiles;
     double predicted_us = 0.0, build_ms = 0.0;
+    int32_t perf_table_loaded = 0;
     // device
     tc::WlDesc* d_desc = nullptr;
     uint32_t* d_row_id = nullptr;
@@ -32,9 +33,18 @@ struct spmv_plan_s {
     int32_t* d_counters = nullptr;
     int64_t device_bytes = 0;
     int sm_count = 0;
+    // streaming kernel (per-warp bulk-copy double buffers)
+    bool stream = true;
+    int32_t stage_slots = 0;                  // slots per warp buffer (largest workload)
+    int stream_grid = 0;
+    int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
 };
 
 namespace tc {
 spmv_status cuda_status(cudaError_t e, const char* what);
+// build the plan (host) and upload it to `device` (capi.cu)
+spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col, const float* val, const spmv_options* opt_in,
+                        int device, spmv_plan_s** out);
 }  // namespace tc

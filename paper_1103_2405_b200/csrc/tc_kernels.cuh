@@ -26,10 +26,20 @@
 #include <stdint.h>
 
 #include "plan.h"
+#include "tc_async.cuh"
 
 namespace tc {
 
-constexpr int kThreads = 768;            // 24 warps per CTA: one CTA per SM at <= 80 registers (no spills)
+#ifndef TC_THREADS
+#define TC_THREADS 512
+#endif
+#ifndef TC_LEAN
+#define TC_LEAN 0          // 1: one unit in flight per lane (few registers, high occupancy)
+#endif
+#ifndef TC_MINB
+#define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
+#endif
+constexpr int kThreads = TC_THREADS;     // threads per CTA of the classic kernel (one CTA per SM)
 constexpr int kWarps = kThreads / 32;
 
 struct TileArgs {
@@ -45,17 +55,31 @@ struct TileArgs {
     int32_t* counters;        // [n_split], zero between launches
 };
 
-__device__ __forceinline__ int4 ld_stream_i4(const int32_t* p) {
+// Slot loads: SMEM = false streams from global memory with evict-first (ld.global.cs); SMEM = true
+// reads slots the bulk-copy ring already placed in shared memory.
+template <bool SMEM> __device__ __forceinline__ int4 ld_i4(const int32_t* p) {
+    if (SMEM) return *reinterpret_cast<const int4*>(p);
     return __ldcs(reinterpret_cast<const int4*>(p));
 }
-__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+template <bool SMEM> __device__ __forceinline__ float4 ld_f4(const float* p) {
+    if (SMEM) return *reinterpret_cast<const float4*>(p);
     return __ldcs(reinterpret_cast<const float4*>(p));
 }
-__device__ __forceinline__ int2 ld_stream_i2(const int32_t* p) {
+template <bool SMEM> __device__ __forceinline__ int2 ld_i2(const int32_t* p) {
+    if (SMEM) return *reinterpret_cast<const int2*>(p);
     return __ldcs(reinterpret_cast<const int2*>(p));
 }
-__device__ __forceinline__ float2 ld_stream_f2(const float* p) {
+template <bool SMEM> __device__ __forceinline__ float2 ld_f2(const float* p) {
+    if (SMEM) return *reinterpret_cast<const float2*>(p);
     return __ldcs(reinterpret_cast<const float2*>(p));
+}
+template <bool SMEM> __device__ __forceinline__ int32_t ld_i1(const int32_t* p) {
+    if (SMEM) return *p;
+    return __ldcs(p);
+}
+template <bool SMEM> __device__ __forceinline__ float ld_f1(const float* p) {
+    if (SMEM) return *p;
+    return __ldcs(p);
 }
 
 template <bool STAGED>
@@ -71,15 +95,15 @@ struct XSrc {
 };
 
 // one vector of KV slots: load cols (+vals), gather x, return the partial dot product
-template <int KV, bool VALUED>
+template <int KV, bool VALUED, bool SMEM>
 struct Unit;
 
-template <bool VALUED>
-struct Unit<4, VALUED> {
+template <bool VALUED, bool SMEM>
+struct Unit<4, VALUED, SMEM> {
     int4 c; float4 v;
     __device__ __forceinline__ void load(const int32_t* col, const float* val, int s) {
-        c = ld_stream_i4(col + s);
-        if (VALUED) v = ld_stream_f4(val + s);
+        c = ld_i4<SMEM>(col + s);
+        if (VALUED) v = ld_f4<SMEM>(val + s);
     }
     template <class X>
     __device__ __forceinline__ float dot(const X& x) const {
@@ -88,12 +112,12 @@ struct Unit<4, VALUED> {
         return (x0 + x1) + (x2 + x3);
     }
 };
-template <bool VALUED>
-struct Unit<2, VALUED> {
+template <bool VALUED, bool SMEM>
+struct Unit<2, VALUED, SMEM> {
     int2 c; float2 v;
     __device__ __forceinline__ void load(const int32_t* col, const float* val, int s) {
-        c = ld_stream_i2(col + s);
-        if (VALUED) v = ld_stream_f2(val + s);
+        c = ld_i2<SMEM>(col + s);
+        if (VALUED) v = ld_f2<SMEM>(val + s);
     }
     template <class X>
     __device__ __forceinline__ float dot(const X& x) const {
@@ -102,12 +126,12 @@ struct Unit<2, VALUED> {
         return x0 + x1;
     }
 };
-template <bool VALUED>
-struct Unit<1, VALUED> {
+template <bool VALUED, bool SMEM>
+struct Unit<1, VALUED, SMEM> {
     int32_t c; float v;
     __device__ __forceinline__ void load(const int32_t* col, const float* val, int s) {
-        c = __ldcs(col + s);
-        if (VALUED) v = __ldcs(val + s);
+        c = ld_i1<SMEM>(col + s);
+        if (VALUED) v = ld_f1<SMEM>(val + s);
     }
     template <class X>
     __device__ __forceinline__ float dot(const X& x) const {
@@ -136,70 +160,92 @@ __device__ __forceinline__ void finish_split(const TileArgs& a, const WlDesc& d,
     }
 }
 
-template <bool VALUED, class X, class Epi>
-__device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const X& x, Epi& epi,
-                                       int lane) {
-    const int w4 = d.w >> 2;                          // int4 groups per row
+// The per-warp work of a workload is a flat sequence of "units" (one vector load per lane);
+// each batch issues UB independent unit loads per lane (8 slots per lane in flight), then the
+// gathers, then the sums; row boundaries fall at fixed unit counts (warp-uniform), where the
+// row is reduced (row major: shuffles inside its lane group) and written.
+//
+// Row major (CSR-vector, L80-L82): lpr lanes per row (power of two covering w/4 int4 units,
+// <= 32), rps = 32/lpr rows per step, upl = ceil(w/4/lpr) units per lane per row.
+// wc / wv: the workload's first slot (global memory, or its copy in shared memory when SMEM).
+template <bool VALUED, bool SMEM, class X, class Epi>
+__device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
+                                       const float* wv, const X& x, Epi& epi, int lane) {
+    constexpr int UB = 2;                                // int4 units per lane per batch
+    const int w4 = d.w >> 2;                             // int4 groups per row
     const int lpr = w4 >= 32 ? 32 : (w4 <= 1 ? 1 : (1 << (32 - __clz(w4 - 1))));
     const int lg = __ffs(lpr) - 1;
     const int rps = 32 >> lg;
     const int sub = lane >> lg, sl = lane & (lpr - 1);
-    for (int r0 = 0; r0 < d.h; r0 += rps) {
-        const int r = r0 + sub;
-        const bool act = r < d.h;
-        uint32_t ent = (act && sl == 0) ? __ldg(a.row_id + d.row_base + r) : PAD_ROW;
-        const int64_t base = d.off + (int64_t)r * d.w;
-        const int32_t* cb = a.col + base;
-        const float* vb = VALUED ? a.val + base : nullptr;
-        const int qend = act ? w4 : 0;
-        float acc = 0.0f;
-        int q = sl;
-        for (; q + lpr < qend; q += 2 * lpr) {
-            Unit<4, VALUED> u0, u1;
-            u0.load(cb, vb, 4 * q);
-            u1.load(cb, vb, 4 * (q + lpr));
-            acc += u0.dot(x) + u1.dot(x);
+    const int upl = (w4 + lpr - 1) >> lg;                // units per lane per row
+    const int steps = (d.h + rps - 1) / rps;
+    const int V = steps * upl;                           // virtual units of this lane
+    float acc = 0.0f;
+    for (int v0 = 0; v0 < V; v0 += UB) {
+        Unit<4, VALUED, SMEM> u[UB];
+        bool ok[UB];
+        #pragma unroll
+        for (int j = 0; j < UB; ++j) {
+            const int v = v0 + j;
+            const int step = v / upl, q = sl + (v - step * upl) * lpr;
+            const int r = step * rps + sub;
+            ok[j] = v < V && r < d.h && q < w4;
+            if (ok[j]) u[j].load(wc + r * d.w, VALUED ? wv + r * d.w : nullptr, 4 * q);
         }
-        if (q < qend) {
-            Unit<4, VALUED> u0;
-            u0.load(cb, vb, 4 * q);
-            acc += u0.dot(x);
-        }
-        for (int o = lpr >> 1; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (act && sl == 0) {
-            if (d.kind == KIND_SPLIT) finish_split(a, d, ent, acc, epi);
-            else epi.write(ent, acc);
+        #pragma unroll
+        for (int j = 0; j < UB; ++j) {
+            const int v = v0 + j;
+            if (v >= V) break;                           // warp-uniform
+            if (ok[j]) acc += u[j].dot(x);
+            if ((v + 1) % upl == 0) {                    // row boundary (warp-uniform)
+                for (int o = lpr >> 1; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                const int r = (v / upl) * rps + sub;
+                if (sl == 0 && r < d.h) {
+                    const uint32_t ent = __ldg(a.row_id + d.row_base + r);
+                    if (d.kind == KIND_SPLIT) finish_split(a, d, ent, acc, epi);
+                    else epi.write(ent, acc);
+                }
+                acc = 0.0f;
+            }
         }
     }
 }
 
-template <int KV, bool VALUED, class X, class Epi>
-__device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const X& x, Epi& epi,
-                                       int lane) {
-    constexpr int UN = KV == 4 ? 2 : 4;               // 32-64 bytes in flight per lane (valued)
-    const int nk = d.w / KV;                          // units per slab
+// Column major (ELL, L84): thread per row over 32-row slabs; the workload is a linear stream of
+// 32*KV-slot units (unit u of lane l at slot u*32*KV + l*KV), a row ends every nk = w/KV units.
+// The row entries (and partial y of accumulating rows) of every row ending in a batch are
+// loaded with the batch.
+template <int KV, bool VALUED, bool SMEM, class X, class Epi>
+__device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
+                                       const float* wv, const X& x, Epi& epi, int lane) {
+    constexpr int UB = (VALUED ? 4 : 8) / KV;            // 4 (valued) / 8 (pattern) slots per lane in flight
+    const int nk = d.w / KV;
     const int slabs = d.h >> 5;
-    const int total = slabs * nk;                     // units (< 2^31: WL-bounded workloads)
+    const int total = slabs * nk;
     const uint32_t* rid = a.row_id + d.row_base + lane;
-    const int32_t* cb = a.col + d.off + lane * KV;
-    const float* vb = VALUED ? a.val + d.off + lane * KV : nullptr;
-    int kk = 0, s = 0;
-    uint32_t ent = slabs > 0 ? __ldg(rid) : PAD_ROW;
+    const int32_t* cb = wc + lane * KV;
+    const float* vb = VALUED ? wv + lane * KV : nullptr;
     float acc = 0.0f;
-    for (int u0 = 0; u0 < total; u0 += UN) {
-        Unit<KV, VALUED> u[UN];
+    for (int u0 = 0; u0 < total; u0 += UB) {
+        Unit<KV, VALUED, SMEM> u[UB];
+        uint32_t ent[UB];
         #pragma unroll
-        for (int j = 0; j < UN; ++j)
-            if (u0 + j < total) u[j].load(cb, vb, (u0 + j) * (32 * KV));
+        for (int j = 0; j < UB; ++j) {
+            const int uu = u0 + j;
+            ent[j] = PAD_ROW;
+            if (uu < total) {
+                u[j].load(cb, vb, uu * (32 * KV));
+                if ((uu + 1) % nk == 0) ent[j] = __ldg(rid + 32 * (uu / nk));
+            }
+        }
         #pragma unroll
-        for (int j = 0; j < UN; ++j) {
-            if (u0 + j < total) {
-                acc += u[j].dot(x);
-                if (++kk == nk) {
-                    if (ent != PAD_ROW) epi.write(ent, acc);
-                    acc = 0.0f; kk = 0; ++s;
-                    ent = s < slabs ? __ldg(rid + 32 * s) : PAD_ROW;
-                }
+        for (int j = 0; j < UB; ++j) {
+            const int uu = u0 + j;
+            if (uu >= total) break;                      // warp-uniform
+            acc += u[j].dot(x);
+            if ((uu + 1) % nk == 0) {                    // row end (warp-uniform)
+                if (ent[j] != PAD_ROW) epi.write(ent[j], acc);
+                acc = 0.0f;
             }
         }
     }
@@ -208,14 +254,59 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
 // zero-length rows (remainder tile): every row of every slab gets value 0
 template <class Epi>
 __device__ __forceinline__ void run_zero(const TileArgs& a, const WlDesc& d, Epi& epi, int lane) {
-    for (int r = lane; r < d.h; r += 32) {
-        uint32_t ent = __ldg(a.row_id + d.row_base + r);
-        if (ent != PAD_ROW) epi.write(ent, 0.0f);
+    for (int r0 = 0; r0 < d.h; r0 += 128) {
+        uint32_t ent[4];
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = r0 + 32 * j + lane;
+            ent[j] = r < d.h ? __ldg(a.row_id + d.row_base + r) : PAD_ROW;
+        }
+        #pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (ent[j] != PAD_ROW) epi.write(ent[j], 0.0f);
     }
 }
 
+template <bool VALUED, bool SMEM, class X, class Epi>
+__device__ __forceinline__ void dispatch_cm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
+                                            const float* wv, const X& x, Epi& epi, int lane) {
+    if (d.kvec == 4) run_cm<4, VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+    else if (d.kvec == 2) run_cm<2, VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+    else run_cm<1, VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+}
+
+__device__ __forceinline__ WlDesc load_desc(const WlDesc* p) {
+    const int4* dp = reinterpret_cast<const int4*>(p);
+    int4 d0 = __ldg(dp), d1 = __ldg(dp + 1);
+    WlDesc d;
+    d.off = (int64_t)(((uint64_t)(uint32_t)d0.y << 32) | (uint32_t)d0.x);
+    d.row_base = d0.z; d.w = d0.w; d.h = d1.x;
+    d.kind = (uint8_t)(d1.y & 0xff); d.kvec = (uint8_t)((d1.y >> 8) & 0xff);
+    d.split_id = d1.z; d.chunk = d1.w;
+    return d;
+}
+
+template <bool VALUED, bool SMEM, class X, class Epi>
+__device__ __forceinline__ void run_workload(const TileArgs& a, const WlDesc& d, const int32_t* wc,
+                                             const float* wv, const X& x, Epi& epi, int lane) {
+    if (d.kind != KIND_CM) run_rm<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+    else if (d.w == 0) run_zero(a, d, epi, lane);
+    else dispatch_cm<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+}
+
+constexpr int kPrefetchAhead = 2;
+
+template <bool VALUED>
+__device__ __forceinline__ void prefetch_workload(const TileArgs& a, int64_t j) {
+    const WlDesc d = load_desc(a.desc + j);
+    const uint32_t bytes = (uint32_t)((int64_t)d.h * d.w * 4 + 15) & ~15u;
+    if (bytes == 0) return;
+    bulk_prefetch_l2(a.col + d.off, bytes);
+    if (VALUED) bulk_prefetch_l2(a.val + d.off, bytes);
+}
+
 template <bool STAGED, bool VALUED, class Epi>
-__global__ void __launch_bounds__(kThreads, 1) tc_spmv_tile(TileArgs a, Epi epi_in) {
+__global__ void __launch_bounds__(kThreads, TC_MINB) tc_spmv_tile(TileArgs a, Epi epi_in) {
     extern __shared__ float xs[];
     Epi epi = epi_in;
     if (!epi.begin()) return;                         // iteration loop already converged
@@ -239,39 +330,106 @@ __global__ void __launch_bounds__(kThreads, 1) tc_spmv_tile(TileArgs a, Epi epi_
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * kWarps;
-    for (int64_t j = a.wl_begin + gw; j < a.wl_end; j += G) {
-        const int4* dp = reinterpret_cast<const int4*>(a.desc + j);
-        int4 d0 = __ldg(dp), d1 = __ldg(dp + 1);
-        WlDesc d;
-        d.off = (int64_t)(((uint64_t)(uint32_t)d0.y << 32) | (uint32_t)d0.x);
-        d.row_base = d0.z; d.w = d0.w; d.h = d1.x;
-        d.kind = (uint8_t)(d1.y & 0xff); d.kvec = (uint8_t)((d1.y >> 8) & 0xff);
-        d.split_id = d1.z; d.chunk = d1.w;
-        if (d.kind != KIND_CM) {
-            run_rm<VALUED>(a, d, x, epi, lane);
-        } else if (d.w == 0) {
-            run_zero(a, d, epi, lane);
-        } else if (d.kvec == 4) {
-            run_cm<4, VALUED>(a, d, x, epi, lane);
-        } else if (d.kvec == 2) {
-            run_cm<2, VALUED>(a, d, x, epi, lane);
-        } else {
-            run_cm<1, VALUED>(a, d, x, epi, lane);
+    // the warp's first workloads: prefetch their slots into L2 (bulk, asynchronous)
+    if (lane == 0) {
+        for (int q = 0; q < kPrefetchAhead; ++q) {
+            const int64_t jn = a.wl_begin + gw + q * G;
+            if (jn < a.wl_end) prefetch_workload<VALUED>(a, jn);
         }
+    }
+    for (int64_t j = a.wl_begin + gw; j < a.wl_end; j += G) {
+        const WlDesc d = load_desc(a.desc + j);
+        // keep kPrefetchAhead workloads of this warp in flight from HBM into L2
+        const int64_t jn = j + (int64_t)kPrefetchAhead * G;
+        if (lane == 0 && jn < a.wl_end) prefetch_workload<VALUED>(a, jn);
+        run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
     }
     epi.end();
 }
 
-// y = A x epilogue-free writer
+constexpr int kStreamThreads = 512;                 // up to 16 warps per CTA
+
+// ---------------------------------------------------------------------------------------------
+// Streaming kernel (default): every warp runs its workloads (round-robin over a persistent grid)
+// out of a private double buffer in shared memory.  While the warp computes workload j from one
+// buffer, its lane 0 has already issued the 1-D bulk copies (cp.async.bulk: the TMA engine,
+// SASS UBLKCP) of the slots of its next workload into the other buffer, completion tracked by an
+// mbarrier.  The slot stream therefore never sits on the warp's dependency chain: HBM latency is
+// hidden by the copy engine, not by registers, and the warp only waits on x gathers (shared
+// memory for dense tiles, L1/L2 for the remainder).  Dense tiles also bulk-copy their x segment.
+struct WsArgs {
+    int32_t buf_slots;          // slots per buffer (>= every workload of the tile, multiple of 4)
+    int32_t x_floats;           // staged x floats (multiple of 4), 0 when not staged
+};
+
+template <bool VALUED>
+__device__ __forceinline__ void ws_issue(const TileArgs& a, const WlDesc& d, int32_t* cbuf,
+                                         float* vbuf, uint64_t* bar, uint64_t pol) {
+    const uint32_t bytes = (uint32_t)((int64_t)d.h * d.w) * 4u;
+    if (bytes == 0) { mbar_arrive(bar); return; }
+    mbar_arrive_expect_tx(bar, VALUED ? 2u * bytes : bytes);
+    bulk_g2s(cbuf, a.col + d.off, bytes, bar, pol);
+    if (VALUED) bulk_g2s(vbuf, a.val + d.off, bytes, bar, pol);
+}
+
+template <bool STAGED, bool VALUED, class Epi>
+__global__ void __launch_bounds__(kStreamThreads, 1) tc_spmv_wstream(TileArgs a, WsArgs s, Epi epi_in) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int nwarps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                 // [nwarps][2] + x
+    uint64_t* xbar = bars + 2 * nwarps;
+    float* xs = reinterpret_cast<float*>(smem + ((2 * nwarps + 1) * 8 + 127) / 128 * 128);
+    const size_t per_buf = (size_t)s.buf_slots * (VALUED ? 2 : 1);
+    int32_t* wb = reinterpret_cast<int32_t*>(xs + s.x_floats) + (size_t)warp * 2 * per_buf;
+    Epi epi = epi_in;
+    if (!epi.begin()) return;                            // iteration loop already converged
+    if (lane == 0) { mbar_init(bars + 2 * warp, 1); mbar_init(bars + 2 * warp + 1, 1); }
+    if (threadIdx.x == 0) mbar_init(xbar, 1);
+    fence_barrier_init();
+    __syncthreads();
+    if (STAGED && threadIdx.x == 0) {
+        mbar_arrive_expect_tx(xbar, (uint32_t)s.x_floats * 4u);
+        bulk_g2s(xs, a.x, (uint32_t)s.x_floats * 4u, xbar, policy_evict_last());
+    }
+    const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+    const int64_t G = (int64_t)gridDim.x * nwarps;
+    const uint64_t pol = policy_evict_first();
+    int32_t* cbuf[2] = {wb, wb + per_buf};
+    float* vbuf[2] = {reinterpret_cast<float*>(wb + s.buf_slots), reinterpret_cast<float*>(wb + per_buf + s.buf_slots)};
+    int64_t j = a.wl_begin + gw;
+    WlDesc d = j < a.wl_end ? load_desc(a.desc + j) : WlDesc{};
+    if (lane == 0 && j < a.wl_end) ws_issue<VALUED>(a, d, cbuf[0], vbuf[0], bars + 2 * warp, pol);
+    if (STAGED) mbar_wait(xbar, 0);
+    XSrc<STAGED> x{a.x, xs, a.width};
+    for (int k = 0; j < a.wl_end; j += G, ++k) {
+        const int cur = k & 1;
+        const int64_t jn = j + G;
+        WlDesc dn = jn < a.wl_end ? load_desc(a.desc + jn) : WlDesc{};
+        if (lane == 0 && jn < a.wl_end) ws_issue<VALUED>(a, dn, cbuf[cur ^ 1], vbuf[cur ^ 1], bars + 2 * warp + (cur ^ 1), pol);
+        mbar_wait(bars + 2 * warp + cur, (uint32_t)(k >> 1) & 1u);
+        run_workload<VALUED, true>(a, d, cbuf[cur], VALUED ? vbuf[cur] : nullptr, x, epi, lane);
+        __syncwarp();                                    // buffer `cur` is refilled two workloads on
+        d = dn;
+    }
+    epi.end();
+}
+
+__host__ __device__ constexpr int ws_bar_bytes(int nwarps) { return ((2 * nwarps + 1) * 8 + 127) / 128 * 128; }
+
+// Epilogue interface: acc_in(ent) returns the partial sum of earlier tiles (0 unless FLAG_ACC),
+// put(ent, v) stores the row's (accumulated) value or applies the fused epilogue,
+// write(ent, v) = put(ent, v + acc_in(ent)).
+// y = A x writer (no epilogue)
 struct EpiStore {
     float* y;
     __device__ __forceinline__ bool begin() { return true; }
     __device__ __forceinline__ void end() {}
-    __device__ __forceinline__ void write(uint32_t ent, float v) {
-        const uint32_t r = ent & ROW_MASK;
-        if (ent & FLAG_ACC) v += y[r];
-        y[r] = v;
+    __device__ __forceinline__ float acc_in(uint32_t ent) const {
+        return (ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f;
     }
+    __device__ __forceinline__ void put(uint32_t ent, float v) { y[ent & ROW_MASK] = v; }
+    __device__ __forceinline__ void write(uint32_t ent, float v) { put(ent, v + acc_in(ent)); }
 };
 
 }  // namespace tc

@@ -1,50 +1,331 @@
-// tune.cpp -- parameter choice.  Explicit options are honoured as given; "auto" values are
-// chosen here (the performance-model auto-tuner replaces the defaults).
+// tune.cpp -- the paper's auto-tuner and performance model (Sec. 3.3, Appendix E), on B200.
+//
+//   offline table   Performance(w, h): whole-GPU slots/s when every warp runs a w x h workload
+//                   (reading R20), measured by bench/calibrate.py for x cached
+//                   (staged in shared memory: dense tiles) and uncached (L1/L2 gathers: the
+//                   remainder, L160), per workload kind and value type
+//   PM(T, WL)       Alg. 3 (L382-L407, Eq. 1-5): walk the tile's packing with workload size WL,
+//                   group workloads into waves of MAX_ACT_WARP warps, t_i = Size_i / P_i with
+//                   P_i the mean table throughput of the wave, total = sum t_i
+//   Partition(T)    Alg. 2 (L358-L375): argmin of PM over the candidate WLs (strict <)
+//   tile count      Alg. 1 (L335-L356): tiles while the first column has >= 2 entries (the
+//                   upper bound), then the count with the least predicted total (B200 model)
+// B200 additions: rows longer than WL are split (R21), so WL candidates
+// are powers of two; each tile launch also pays a launch gap, the staging of its x segment
+// (dense tiles) and the read-modify-write of y for rows an earlier tile touched.
 #include "tune.h"
 
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+#include <string>
 
 #include "plan_impl.h"
 
 namespace tc {
 
-static constexpr int32_t kDefaultTileWidth = 24576;   // 96 KB of x per CTA: 2 CTAs per SM
+static constexpr int32_t kDefaultTileWidth = 24576;
 static constexpr int32_t kDefaultWL = 1024;
 
+// ------------------------------------------------------------------ offline table
+struct PerfTable {
+    // key: (cached, valued, kind) -> grid over (log2 w, log2 h)
+    struct Grid { std::vector<double> lw, lh; std::vector<std::vector<double>> v; };
+    std::map<int, Grid> grids;
+    double launch_us = 3.0;         // per tile launch gap
+    double stage_GBps = 6000.0;     // chip-wide L2 -> shared memory staging bandwidth
+    double rmw_GBps = 4000.0;       // y read-modify-write of accumulating rows
+    int max_act_warp = 148 * 32;
+    bool loaded = false;
+    std::string source = "built-in";
+
+    static int key(bool cached, bool valued, int kind) { return (cached ? 4 : 0) + (valued ? 2 : 0) + (kind == KIND_CM ? 1 : 0); }
+
+    // bilinear interpolation in (log2 w, log2 h), clamped to the measured range
+    double lookup(bool cached, bool valued, int kind, double w, double h) const {
+        auto it = grids.find(key(cached, valued, kind));
+        if (it == grids.end() || it->second.lw.empty() || it->second.lh.empty()) return analytic(cached, valued, kind, w, h);
+        const Grid& g = it->second;
+        auto locate = [](const std::vector<double>& ax, double v, int& i, double& f) {
+            if (v <= ax.front()) { i = 0; f = 0; return; }
+            if (v >= ax.back()) { i = (int)ax.size() - 1; f = 0; return; }
+            i = (int)(std::upper_bound(ax.begin(), ax.end(), v) - ax.begin()) - 1;
+            f = (v - ax[i]) / (ax[i + 1] - ax[i]);
+        };
+        int i, j; double fi, fj;
+        locate(g.lw, std::log2(std::max(w, 1.0)), i, fi);
+        locate(g.lh, std::log2(std::max(h, 1.0)), j, fj);
+        auto at = [&](int a, int b) {
+            a = std::min(a, (int)g.lw.size() - 1); b = std::min(b, (int)g.lh.size() - 1);
+            return g.v[a][b];
+        };
+        double v00 = at(i, j), v10 = at(i + 1, j), v01 = at(i, j + 1), v11 = at(i + 1, j + 1);
+        if (fi == 0) { v10 = v00; v11 = v01; }
+        if (fj == 0) { v01 = v00; v11 = v10; }
+        double v = (1 - fi) * (1 - fj) * v00 + fi * (1 - fj) * v10 + (1 - fi) * fj * v01 + fi * fj * v11;
+        return v > 0 ? v : analytic(cached, valued, kind, w, h);
+    }
+    // used only when no measured table is available: slots/s bounded by HBM streaming and by
+    // the gather rate (shared memory ~1.3 T/s, L1/L2 ~0.27 T/s)
+    static double analytic(bool cached, bool valued, int kind, double w, double h) {
+        const double bytes = valued ? 8.0 : 4.0;
+        const double hbm = 6.4e12 / bytes;
+        const double gather = cached ? 1.3e12 : 2.7e11;
+        double eff = 1.0;
+        if (kind == KIND_RM) eff = std::min(1.0, w / 128.0 + 0.25);
+        else eff = std::min(1.0, 0.5 + w / 32.0);
+        (void)h;
+        return eff * std::min(hbm, gather);
+    }
+};
+
+static bool parse_table(const std::string& text, PerfTable& T) {
+    // minimal reader for the calibration file: "key": number and "entries": [[c,v,k,w,h,s],...]
+    auto num_after = [&](const char* k, double& out) {
+        size_t p = text.find(std::string("\"") + k + "\"");
+        if (p == std::string::npos) return false;
+        p = text.find(':', p);
+        if (p == std::string::npos) return false;
+        out = std::strtod(text.c_str() + p + 1, nullptr);
+        return true;
+    };
+    double v;
+    if (num_after("launch_us", v)) T.launch_us = v;
+    if (num_after("stage_GBps", v)) T.stage_GBps = v;
+    if (num_after("rmw_GBps", v)) T.rmw_GBps = v;
+    if (num_after("max_act_warp", v)) T.max_act_warp = (int)v;
+    size_t p = text.find("\"entries\"");
+    if (p == std::string::npos) return false;
+    p = text.find('[', p);
+    if (p == std::string::npos) return false;
+    std::map<int, std::map<std::pair<double, double>, double>> raw;
+    const char* s = text.c_str() + p + 1;
+    int n = 0;
+    while (*s) {
+        while (*s && *s != '[' && *s != ']') ++s;
+        if (!*s || *s == ']') break;
+        ++s;
+        double f[6];
+        int k = 0;
+        while (k < 6 && *s && *s != ']') {
+            while (*s == ' ' || *s == ',' || *s == '\n') ++s;
+            char* e = nullptr;
+            f[k] = std::strtod(s, &e);
+            if (e == s) return false;
+            s = e;
+            ++k;
+        }
+        while (*s && *s != ']') ++s;
+        if (*s) ++s;
+        if (k != 6) return false;
+        raw[PerfTable::key(f[0] != 0, f[1] != 0, (int)f[2])][{std::log2(f[3]), std::log2(f[4])}] = f[5];
+        ++n;
+    }
+    for (auto& kv : raw) {
+        PerfTable::Grid g;
+        for (auto& e : kv.second) { g.lw.push_back(e.first.first); g.lh.push_back(e.first.second); }
+        std::sort(g.lw.begin(), g.lw.end()); g.lw.erase(std::unique(g.lw.begin(), g.lw.end()), g.lw.end());
+        std::sort(g.lh.begin(), g.lh.end()); g.lh.erase(std::unique(g.lh.begin(), g.lh.end()), g.lh.end());
+        g.v.assign(g.lw.size(), std::vector<double>(g.lh.size(), 0.0));
+        // fill: nearest measured neighbour in h for holes (rm shapes need w >= h)
+        for (size_t i = 0; i < g.lw.size(); ++i)
+            for (size_t j = 0; j < g.lh.size(); ++j) {
+                double best = 0, bd = 1e30;
+                for (auto& e : kv.second) {
+                    double d = std::fabs(e.first.first - g.lw[i]) * 4 + std::fabs(e.first.second - g.lh[j]);
+                    if (d < bd) { bd = d; best = e.second; }
+                }
+                g.v[i][j] = best;
+            }
+        T.grids[kv.first] = g;
+    }
+    return n > 0;
+}
+
+static const PerfTable& table_for(const char* path_opt) {
+    static PerfTable builtin;
+    static std::map<std::string, PerfTable> cache;
+    std::string path = path_opt ? path_opt : "";
+    if (path.empty()) {
+        const char* env = std::getenv("TCSPMV_PERF_TABLE");
+        if (env) path = env;
+    }
+    if (path.empty()) {
+        Dl_info info;
+        if (dladdr((void*)&table_for, &info) && info.dli_fname) {
+            std::string so = info.dli_fname;
+            size_t k = so.rfind('/');
+            std::string dir = k == std::string::npos ? "." : so.substr(0, k);
+            path = dir + "/../data/perf_table_b200.json";
+        }
+    }
+    auto it = cache.find(path);
+    if (it != cache.end()) return it->second;
+    std::ifstream f(path);
+    if (!f) return builtin;
+    std::stringstream ss;
+    ss << f.rdbuf();
+    PerfTable T;
+    if (!parse_table(ss.str(), T)) return builtin;
+    T.loaded = true;
+    T.source = path;
+    return cache.emplace(path, T).first->second;
+}
+
+// ------------------------------------------------------------------ Alg. 3 on the packing walk
+// hist: (length, count) pairs, lengths descending (a tile's ranked rows).  Walks the same packing
+// rules as pack_layout and charges every workload to its wave.
+static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int64_t WL, int align,
+                      bool split, int ell_h, bool cached, bool valued, const PerfTable& T,
+                      int64_t* n_workloads = nullptr) {
+    const int64_t M = std::max(1, T.max_act_warp);      // MAX_ACT_WARP (Eq. 1)
+    double total = 0.0, P = 0.0, S = 0.0;
+    int64_t cnt = 0, nw = 0;
+    auto add = [&](int kind, int64_t w, int64_t h, int64_t slots) {   // Alg. 3 lines 11-14
+        P += T.lookup(cached, valued, kind, (double)std::max<int64_t>(w, 1), (double)h);
+        S += (double)slots;
+        ++cnt; ++nw;
+        if (cnt == M) { total += S / (P / (double)cnt); P = S = 0.0; cnt = 0; }   // Eq. 3-5
+    };
+    auto rup = [](int64_t a, int64_t b) { return (a + b - 1) / b * b; };
+    // cursor over the ranked rows, stored as (length, count) groups
+    size_t g = 0;
+    int64_t off = 0, remaining = 0;
+    for (auto& h : hist) remaining += h.second;
+    auto advance = [&](int64_t k) {
+        remaining -= k;
+        while (k > 0 && g < hist.size()) {
+            const int64_t c = std::min(k, hist[g].second - off);
+            off += c; k -= c;
+            if (off == hist[g].second) { ++g; off = 0; }
+        }
+    };
+    while (remaining > 0) {                                  // Alg. 3 lines 7-16 (packing walk)
+        const int64_t w = hist[g].first;
+        const int64_t hq = std::max<int64_t>(1, WL / std::max<int64_t>(w, 1));
+        if (split && w > WL) {                               // R21: one-row chunks
+            for (int64_t c = 0; c * WL < w; ++c) {
+                const int64_t part = std::min<int64_t>(WL, w - c * WL), wp = rup(part, align);
+                add(KIND_RM, wp, 1, wp);
+            }
+            advance(1);
+        } else if (w >= hq) {                                // row major
+            const int64_t h = std::min<int64_t>(hq, remaining), wp = rup(w, align);
+            add(KIND_RM, wp, h, h * wp);
+            advance(h);
+        } else {                                             // column major
+            const int64_t take = std::min<int64_t>(rup(hq, ell_h), remaining);
+            const int64_t hs = rup(take, ell_h);
+            add(KIND_CM, w, hs, hs * w);
+            advance(take);
+        }
+    }
+    if (cnt > 0) total += S / (P / (double)cnt);             // last (partial) wave, R23
+    if (n_workloads) *n_workloads = nw;
+    return total;   // seconds
+}
+
+// Alg. 2 in B200 mode: candidates are powers of two (rows longer than WL split) plus the paper's
+// multiples of the longest row; paper mode (no split) keeps WL >= the longest row.
+static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, const BuildParams& bp,
+                           bool cached, bool valued, const PerfTable& T, int32_t& opt_wl, double& opt_t) {
+    const int64_t L = hist.empty() ? 1 : std::max<int64_t>(1, hist[0].first);
+    int64_t nnz = 0;
+    for (auto& h : hist) nnz += h.first * h.second;
+    std::vector<int64_t> cand;
+    if (bp.split) {
+        for (int64_t c = 128; c <= 4096; c *= 2) cand.push_back(c);
+    } else {
+        const int64_t up = std::max<int64_t>(L, nnz / std::max(1, T.max_act_warp));
+        for (int64_t c = L; c <= up && cand.size() < 64; c += L) cand.push_back(c);
+        if (cand.empty()) cand.push_back(L);
+    }
+    opt_t = INFINITY; opt_wl = (int32_t)cand[0];
+    for (int64_t c : cand) {
+        double t = pm_tile(hist, c, bp.align_rm, bp.split, bp.ell_h, cached, valued, T);
+        if (t < opt_t) { opt_t = t; opt_wl = (int32_t)c; }
+    }
+}
+
+struct Choice { int32_t tw, T; std::vector<int32_t> wl; std::vector<double> us; double total; };
+
+static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildParams& base, int32_t tw,
+                       int32_t T, const PerfTable& tab) {
+    Choice c{tw, T, {}, {}, 0.0};
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> hist;
+    tile_histograms(P, tw, T, hist);
+    const bool valued = !P.pattern;
+    for (int32_t t = 0; t <= T; ++t) {
+        const bool cached = t < T && opt.stage_x != 0;
+        int32_t wl = kDefaultWL;
+        double sec = 0.0;
+        if (opt.workload_sizes) wl = opt.workload_sizes[std::min(t, opt.num_tiles >= 0 ? opt.num_tiles : t)];
+        else if (opt.workload_size > 0) wl = opt.workload_size;
+        if (opt.workload_sizes || opt.workload_size > 0) {
+            BuildParams b = base; b.wl.assign(1, wl);
+            sec = pm_tile(hist[t], wl, b.align_rm, b.split, b.ell_h, cached, valued, tab);
+        } else {
+            partition_tile(hist[t], base, cached, valued, tab, wl, sec);
+        }
+        int64_t rows = 0, nnz = 0;
+        for (auto& h : hist[t]) { rows += h.second; nnz += h.first * h.second; }
+        double us = sec * 1e6;
+        if (rows > 0) {
+            us += tab.launch_us;
+            if (cached) us += (double)tw * 4.0 * 148 / (tab.stage_GBps * 1e3);
+            if (t > 0) us += (double)rows * 8.0 / (tab.rmw_GBps * 1e3);   // y partial read + write
+        }
+        c.wl.push_back(wl);
+        c.us.push_back(us);
+        c.total += us;
+    }
+    return c;
+}
+
 spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_count,
-                          BuildParams& bp, std::vector<double>& pred_us) {
-    (void)sm_count;
+                          BuildParams& bp, std::vector<double>& pred_us, int32_t* table_loaded) {
     bp.align_rm = opt.align_rm;
     bp.split = opt.split_long_rows != 0;
     bp.camping = opt.camping_pad != 0;
     bp.ell_h = opt.ell_h;
-    bp.tile_width = opt.tile_width > 0 ? opt.tile_width : kDefaultTileWidth;
-    const int64_t max_tiles = P.n_cols > 0 ? (P.n_cols + bp.tile_width - 1) / bp.tile_width : 0;
-    if (opt.num_tiles >= 0) {
-        // explicit counts are clipped to the tiles that exist (ceil(n_cols / tile_width))
-        bp.num_tiles = (int32_t)std::min<int64_t>(opt.num_tiles, max_tiles);
-    } else {
-        bp.num_tiles = std::min<int32_t>(paper_tile_count(P, bp.tile_width), 2);
-    }
-    if (bp.num_tiles > 63) { set_error("more than 63 dense tiles"); return SPMV_ERANGE; }
-    const int32_t T = bp.num_tiles;
-    bp.wl.assign(T + 1, kDefaultWL);
-    if (opt.workload_sizes) {
-        // num_tiles + 1 values as given; after clipping the remainder keeps the last value
-        for (int32_t t = 0; t < T; ++t) bp.wl[t] = opt.workload_sizes[t];
-        bp.wl[T] = opt.workload_sizes[opt.num_tiles >= 0 ? opt.num_tiles : T];
-    } else if (opt.workload_size > 0) {
-        std::fill(bp.wl.begin(), bp.wl.end(), opt.workload_size);
-    } else if (!bp.split) {
-        // paper lower bound (Alg. 2 line 3): WL >= the tile's longest row
-        std::vector<std::vector<std::pair<int64_t, int64_t>>> hist;
-        tile_histograms(P, bp.tile_width, T, hist);
-        for (int32_t t = 0; t <= T; ++t) {
-            int64_t L = hist[t].empty() ? 1 : std::max<int64_t>(1, hist[t][0].first);
-            bp.wl[t] = (int32_t)std::max<int64_t>(kDefaultWL, L);
+    PerfTable tab = table_for(opt.perf_table_path);
+    tab.max_act_warp = std::max(1, tab.max_act_warp / 148 * sm_count);
+    if (opt.perf_table_path && !tab.loaded) { set_error("performance table unreadable"); return SPMV_ETABLE; }
+    if (table_loaded) *table_loaded = tab.loaded ? 1 : 0;
+
+    std::vector<int32_t> tws;
+    if (opt.tile_width > 0) tws.push_back(opt.tile_width);
+    else tws = {12288, 24576, 49152};
+    Choice best{0, 0, {}, {}, INFINITY};
+    for (int32_t tw : tws) {
+        const int64_t max_tiles = P.n_cols > 0 ? (P.n_cols + tw - 1) / tw : 0;
+        std::vector<int32_t> Ts;
+        if (opt.num_tiles >= 0) Ts.push_back((int32_t)std::min<int64_t>(opt.num_tiles, max_tiles));
+        else {
+            // Alg. 1 gives the upper bound; the model picks the count (B200 terms included)
+            const int32_t Tp = std::min<int32_t>(paper_tile_count(P, tw), 16);
+            for (int32_t T = 0; T <= Tp; T = (T < 4 ? T + 1 : T * 2)) Ts.push_back(T);
+            if (Ts.back() != Tp) Ts.push_back(Tp);
         }
+        for (int32_t T : Ts) {
+            if (T > 63) continue;
+            Choice c = evaluate(P, opt, bp, tw, T, tab);
+            if (c.total < best.total) best = c;
+        }
+        if (opt.num_tiles >= 0 && opt.tile_width > 0) break;
     }
-    pred_us.assign(T + 1, 0.0);
+    if (best.wl.empty()) { set_error("no tiling candidate"); return SPMV_EINVAL; }
+    bp.tile_width = best.tw;
+    bp.num_tiles = best.T;
+    bp.wl = best.wl;
+    pred_us = best.us;
     return SPMV_OK;
 }
 

@@ -10,7 +10,7 @@ struct spmv_plan_s;
 namespace tc {
 
 spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_count,
-                          BuildParams& bp, std::vector<double>& pred_us);
+                          BuildParams& bp, std::vector<double>& pred_us, int32_t* table_loaded = nullptr);
 void predict_plan(spmv_plan_s& p, const std::vector<double>& pred_us);
 
 }  // namespace tc

@@ -56,8 +56,13 @@ def test_hits_parity(opt, gpu):
             info = s.run()
             a, h = s.result()
             ra, rh, r = oracle.hits(G.n, G.row_ptr, G.col, norm=norm, fixed_iters=info["iterations"])
-            err = np.abs(a - ra).sum() + np.abs(h - rh).sum()
-            assert err < 2 * L1_BAR, (name, norm, err, info)
+            err_a, err_h = np.abs(a - ra).sum(), np.abs(h - rh).sum()
+            # paper normalisation (halves sum to 1, L440): 1e-6 L1 per vector.  Unit-L2 halves have
+            # L1 norm up to sqrt(n), beyond fp32 resolution at 1e-6 absolute: the bar is scaled by
+            # each reference vector's L1 norm (R3).
+            bar_a = L1_BAR * (1.0 if norm == 1 else np.abs(ra).sum())
+            bar_h = L1_BAR * (1.0 if norm == 1 else np.abs(rh).sum())
+            assert err_a < bar_a and err_h < bar_h, (name, norm, err_a, err_h, info)
 
 
 @pytest.mark.parametrize("opt", range(len(OPTS)))

@@ -1,0 +1,84 @@
+"""Row-partitioned (multi-GPU) host logic on CPU: the library's bitonic partition equals the
+oracle's snake order (reading R25), the slot layout is consistent, and a world-2
+gloo run of the exchange protocol (each rank computes its own rows, one allgather of the slots)
+reproduces the single-process product."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import graphgen
+import oracle
+from oracle import partition_ref
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+def test_bitonic_matches_oracle(P):
+    from paper_1103_2405_b200 import bitonic_partition, partition_plan
+    rng = np.random.default_rng(P)
+    lens = rng.zipf(1.8, 2001).astype(np.int64)
+    own = bitonic_partition(lens, P)
+    assert own.tolist() == partition_ref.bitonic_partition(lens.tolist(), P)
+    owner, lidx, S = partition_plan(lens, P)
+    assert np.array_equal(owner, own)
+    counts = np.bincount(owner, minlength=P)
+    assert counts.max() - counts.min() <= 1 and S == counts.max()
+    for r in range(P):                       # local index = rank of the row among its owner's rows
+        rows = np.nonzero(owner == r)[0]
+        assert np.array_equal(lidx[rows], np.arange(len(rows)))
+
+
+def test_partition_errors():
+    from paper_1103_2405_b200 import SpmvError, bitonic_partition
+    with pytest.raises(SpmvError, match="ERANGE"):
+        bitonic_partition([1, 2], 3)
+    with pytest.raises(SpmvError, match="EINVAL"):
+        bitonic_partition([1, 2], 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, result_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1103_2405_b200 import partition_plan
+    G = graphgen.make_graph("t_small")
+    rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)      # PageRank matrix A^T
+    rl = np.diff(rp)
+    owner, lidx, S = partition_plan(rl, world)
+    x = graphgen.uniform_f32(G.n, seed=3)
+    # this rank's rows, computed locally (the oracle stands in for the local SpMV)
+    mine = np.nonzero(owner == rank)[0]
+    sub_rp = np.concatenate([[0], np.cumsum(rl[mine])]).astype(np.int64)
+    sub_col = np.concatenate([col[rp[r]:rp[r + 1]] for r in mine]) if len(mine) else np.zeros(0, np.int32)
+    y_loc, _ = oracle.spmv(sub_rp, sub_col, None, x)
+    slot = np.zeros(S, np.float64)
+    slot[lidx[mine]] = y_loc
+    gathered = [torch.zeros(S, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(gathered, torch.from_numpy(slot))
+    G_all = torch.cat(gathered).numpy()
+    y = G_all[owner.astype(np.int64) * S + lidx]                     # gpos = owner * S + local
+    np.save(os.path.join(result_dir, f"y{rank}.npy"), y)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_exchange_protocol(world, tmp_path):
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    G = graphgen.make_graph("t_small")
+    rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)
+    ref, _ = oracle.spmv(rp, col, None, graphgen.uniform_f32(G.n, seed=3))
+    for r in range(world):
+        y = np.load(tmp_path / f"y{r}.npy")
+        assert np.array_equal(y, ref)          # every rank holds the identical full vector
