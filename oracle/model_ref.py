@@ -73,3 +73,48 @@ def tile_count(collen_sorted, n_cols: int, tile_width: int) -> int:
             break
         nt += 1
     return nt
+
+
+def _rup(a, b):
+    return (a + b - 1) // b * b
+
+
+def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32):
+    """B200 reading of Alg. 3: the same wave model (Eq. 1-5) charged over
+    the workloads the format actually builds (the packing of Solution 3 / format_ref with row
+    splitting, R21, and clipping, R13), each looked up at its padded shape.
+    hist: [(row length, count)] with lengths descending.  perf(kind, w, h) -> slots/s.
+    Returns seconds."""
+    rows = []
+    for length, count in hist:
+        rows += [length] * count
+    waves = []                                   # per wave: [sum perf, sum size, count]
+    def add(kind, w, h, size):
+        if not waves or waves[-1][2] == max_act_warp:
+            waves.append([0.0, 0.0, 0])
+        wv = waves[-1]
+        wv[0] += perf(kind, max(w, 1), h)
+        wv[1] += size
+        wv[2] += 1
+    i = 0
+    while i < len(rows):
+        w = rows[i]
+        hq = max(1, WL // max(w, 1))
+        if split and w > WL:
+            c = 0
+            while c * WL < w:
+                wp = _rup(min(WL, w - c * WL), align)
+                add("rm", wp, 1, wp)
+                c += 1
+            i += 1
+        elif w >= hq:
+            h = min(hq, len(rows) - i)
+            wp = _rup(w, align)
+            add("rm", wp, h, h * wp)
+            i += h
+        else:
+            take = min(_rup(hq, ell_h), len(rows) - i)
+            hs = _rup(take, ell_h)
+            add("cm", w, hs, hs * w)
+            i += take
+    return sum(S / (P / c) for P, S, c in waves)

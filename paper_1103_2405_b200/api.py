@@ -179,6 +179,7 @@ class Solver:
 
     def __init__(self, algo: str, n, row_ptr, col, device=0, comm=None, iter_kw=None, **options):
         self.algo, self.n = algo, int(n)
+        self._comm = comm                      # the communicator must outlive the solver
         rp = _np(row_ptr, np.int64)
         cl = _np(col, np.int32)
         self.m = int(rp[-1])

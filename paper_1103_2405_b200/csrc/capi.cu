@@ -130,7 +130,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
         const char* kenv = std::getenv("TCSPMV_KERNEL");
-        p->stream = !(kenv && std::string(kenv) == "classic");
+        p->stream = kenv && std::string(kenv) == "stream";
         if (p->stream && (e = build_stream_tables(p))) {
             free_device(p); delete p; return cuda_status(e, "stage tables");
         }

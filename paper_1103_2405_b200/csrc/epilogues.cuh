@@ -92,21 +92,26 @@ struct EpiAffine {
         res = 0.0; dm = 0.0;
         return true;
     }
-    __device__ __forceinline__ float acc_in(uint32_t ent) const {
-        return (ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f;
-    }
-    __device__ __forceinline__ void write(uint32_t ent, float v) { put(ent, v + acc_in(ent)); }
-    __device__ __forceinline__ void put(uint32_t ent, float v) {
+    struct Pre { float acc, p_old, inv; };
+    __device__ __forceinline__ Pre prefetch(uint32_t ent) const {
+        Pre q{0.0f, 0.0f, 0.0f};
+        if (ent == PAD_ROW) return q;
         const uint32_t r = ent & ROW_MASK;
+        if (ent & FLAG_ACC) q.acc = y[r];
+        if (ent & FLAG_FINAL) { q.p_old = p[r]; q.inv = __ldg(inv_deg + r); }
+        return q;
+    }
+    __device__ __forceinline__ void write(uint32_t ent, float v) { commit(ent, v, prefetch(ent)); }
+    __device__ __forceinline__ void commit(uint32_t ent, float v, const Pre& pre) {
+        const uint32_t r = ent & ROW_MASK;
+        v += pre.acc;
         if (!(ent & FLAG_FINAL)) { y[r] = v; return; }
         float pn = fmaf(c, v, tele);
         if (rwr && (int32_t)r == q) pn += 1.0f - c;
-        const float po = p[r];
-        res += fabs((double)pn - (double)po);
+        res += fabs((double)pn - (double)pre.p_old);
         p[r] = pn;
-        const float id = __ldg(inv_deg + r);
-        z_next[r] = pn * id;
-        if (id == 0.0f) dm += (double)pn;
+        z_next[r] = pn * pre.inv;
+        if (pre.inv == 0.0f) dm += (double)pn;
     }
     __device__ __forceinline__ void end() {
         double v[2] = {res, dm};
@@ -141,16 +146,23 @@ struct EpiHitsSpmv {
         s0 = 0.0; s1 = 0.0;
         return true;
     }
-    __device__ __forceinline__ float acc_in(uint32_t ent) const {
-        return (ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f;
-    }
-    __device__ __forceinline__ void write(uint32_t ent, float v) { put(ent, v + acc_in(ent)); }
-    __device__ __forceinline__ void put(uint32_t ent, float v) {
+    struct Pre { float acc; int half; };
+    __device__ __forceinline__ Pre prefetch(uint32_t ent) const {
+        Pre q{0.0f, 0};
+        if (ent == PAD_ROW) return q;
         const uint32_t r = ent & ROW_MASK;
+        if (ent & FLAG_ACC) q.acc = y[r];
+        if (ent & FLAG_FINAL) q.half = __ldg(half + r);
+        return q;
+    }
+    __device__ __forceinline__ void write(uint32_t ent, float v) { commit(ent, v, prefetch(ent)); }
+    __device__ __forceinline__ void commit(uint32_t ent, float v, const Pre& pre) {
+        const uint32_t r = ent & ROW_MASK;
+        v += pre.acc;
         y[r] = v;
         if (!(ent & FLAG_FINAL)) return;
         const double d = l2 ? (double)v * (double)v : fabs((double)v);
-        if (__ldg(half + r)) s1 += d; else s0 += d;
+        if (pre.half) s1 += d; else s0 += d;
     }
     __device__ __forceinline__ void end() {
         double v[2] = {s0, s1};

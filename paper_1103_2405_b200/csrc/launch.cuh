@@ -42,16 +42,19 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
         size_t smem = 0;
         int threads = 0;
         bool staged = ti.staged != 0;
+        bool fits = true;
         if (staged && !ws_geometry(p, t, true, s, smem, threads)) staged = false;
-        if (!staged && !ws_geometry(p, t, false, s, smem, threads)) return cudaErrorInvalidConfiguration;
-        if (staged) {
+        if (!staged && !ws_geometry(p, t, false, s, smem, threads)) fits = false;
+        if (!fits) {
+            // workloads too large for per-warp buffers: this tile runs the classic kernel
+        } else if (staged) {
             if (p.pattern) tc_spmv_wstream<true, false, Epi><<<p.stream_grid, threads, smem, st>>>(a, s, epi);
             else tc_spmv_wstream<true, true, Epi><<<p.stream_grid, threads, smem, st>>>(a, s, epi);
         } else {
             if (p.pattern) tc_spmv_wstream<false, false, Epi><<<p.stream_grid, threads, smem, st>>>(a, s, epi);
             else tc_spmv_wstream<false, true, Epi><<<p.stream_grid, threads, smem, st>>>(a, s, epi);
         }
-        return cudaGetLastError();
+        if (fits) return cudaGetLastError();
     }
     if (ti.staged) {
         size_t smem = (size_t)a.width * sizeof(float);
@@ -81,20 +84,6 @@ cudaError_t launch_tiles(const spmv_plan_s& p, const std::vector<int>& grids, co
 template <class Epi>
 cudaError_t setup_grids(spmv_plan_s& p, std::vector<int>& grids) {
     cudaError_t e;
-    if (p.stream) {
-        int optin = 0;
-        if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device))) return e;
-        auto k0 = p.pattern ? tc_spmv_wstream<true, false, Epi> : tc_spmv_wstream<true, true, Epi>;
-        auto k1 = p.pattern ? tc_spmv_wstream<false, false, Epi> : tc_spmv_wstream<false, true, Epi>;
-        cudaFuncAttributes fa0, fa1;
-        if ((e = cudaFuncGetAttributes(&fa0, k0)) || (e = cudaFuncGetAttributes(&fa1, k1))) return e;
-        const int dyn = optin - (int)std::max(fa0.sharedSizeBytes, fa1.sharedSizeBytes);
-        if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)) ||
-            (e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return e;
-        p.max_dyn_smem = std::min(p.max_dyn_smem > 0 ? p.max_dyn_smem : dyn, dyn);
-        grids.assign(p.num_tiles + 1, p.stream_grid);
-        return cudaSuccess;
-    }
     auto kst = p.pattern ? tc_spmv_tile<true, false, Epi> : tc_spmv_tile<true, true, Epi>;
     auto kgl = p.pattern ? tc_spmv_tile<false, false, Epi> : tc_spmv_tile<false, true, Epi>;
     int optin = 0;
@@ -114,6 +103,19 @@ cudaError_t setup_grids(spmv_plan_s& p, std::vector<int>& grids) {
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kst, kThreads, smem))) return e;
         if (nb < 1) { p.tiles[t].staged = 0; continue; }
         grids[t] = nb * p.sm_count;
+    }
+    if (p.stream) {  // classic attributes above stay set: tiles that do not fit fall back
+        int optin = 0;
+        if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device))) return e;
+        auto k0 = p.pattern ? tc_spmv_wstream<true, false, Epi> : tc_spmv_wstream<true, true, Epi>;
+        auto k1 = p.pattern ? tc_spmv_wstream<false, false, Epi> : tc_spmv_wstream<false, true, Epi>;
+        cudaFuncAttributes fa0, fa1;
+        if ((e = cudaFuncGetAttributes(&fa0, k0)) || (e = cudaFuncGetAttributes(&fa1, k1))) return e;
+        const int dyn = optin - (int)std::max(fa0.sharedSizeBytes, fa1.sharedSizeBytes);
+        if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)) ||
+            (e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return e;
+        p.max_dyn_smem = std::min(p.max_dyn_smem > 0 ? p.max_dyn_smem : dyn, dyn);
+        grids.assign(p.num_tiles + 1, p.stream_grid);
     }
     return cudaSuccess;
 }

@@ -33,8 +33,14 @@ namespace tc {
 #ifndef TC_THREADS
 #define TC_THREADS 512
 #endif
-#ifndef TC_LEAN
-#define TC_LEAN 0          // 1: one unit in flight per lane (few registers, high occupancy)
+#ifndef TC_RM_UB
+#define TC_RM_UB 1         // row major: int4 units per lane per batch
+#endif
+#ifndef TC_CM_SLOTS_V
+#define TC_CM_SLOTS_V 2    // column major, valued: slots per lane per batch
+#endif
+#ifndef TC_CM_SLOTS_P
+#define TC_CM_SLOTS_P 2    // column major, pattern: slots per lane per batch
 #endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
@@ -171,7 +177,7 @@ __device__ __forceinline__ void finish_split(const TileArgs& a, const WlDesc& d,
 template <bool VALUED, bool SMEM, class X, class Epi>
 __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
                                        const float* wv, const X& x, Epi& epi, int lane) {
-    constexpr int UB = 2;                                // int4 units per lane per batch
+    constexpr int UB = TC_RM_UB;                         // int4 units per lane per batch
     const int w4 = d.w >> 2;                             // int4 groups per row
     const int lpr = w4 >= 32 ? 32 : (w4 <= 1 ? 1 : (1 << (32 - __clz(w4 - 1))));
     const int lg = __ffs(lpr) - 1;
@@ -181,9 +187,13 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
     const int steps = (d.h + rps - 1) / rps;
     const int V = steps * upl;                           // virtual units of this lane
     float acc = 0.0f;
+    uint32_t ent_open = PAD_ROW;
+    typename Epi::Pre pre_open{};
     for (int v0 = 0; v0 < V; v0 += UB) {
         Unit<4, VALUED, SMEM> u[UB];
         bool ok[UB];
+        uint32_t ent_s[UB];
+        typename Epi::Pre pre_s[UB];
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int v = v0 + j;
@@ -191,19 +201,23 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
             const int r = step * rps + sub;
             ok[j] = v < V && r < d.h && q < w4;
             if (ok[j]) u[j].load(wc + r * d.w, VALUED ? wv + r * d.w : nullptr, 4 * q);
+            // a row's entry and its epilogue operands are fetched when the row starts, so their
+            // latency overlaps the row's slot loads and gathers
+            ent_s[j] = (v < V && v % upl == 0 && sl == 0 && r < d.h) ? __ldg(a.row_id + d.row_base + r) : PAD_ROW;
         }
+        #pragma unroll
+        for (int j = 0; j < UB; ++j) pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j]);
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int v = v0 + j;
             if (v >= V) break;                           // warp-uniform
+            if (v % upl == 0) { ent_open = ent_s[j]; pre_open = pre_s[j]; }
             if (ok[j]) acc += u[j].dot(x);
             if ((v + 1) % upl == 0) {                    // row boundary (warp-uniform)
                 for (int o = lpr >> 1; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                const int r = (v / upl) * rps + sub;
-                if (sl == 0 && r < d.h) {
-                    const uint32_t ent = __ldg(a.row_id + d.row_base + r);
-                    if (d.kind == KIND_SPLIT) finish_split(a, d, ent, acc, epi);
-                    else epi.write(ent, acc);
+                if (ent_open != PAD_ROW) {
+                    if (d.kind == KIND_SPLIT) finish_split(a, d, ent_open, acc, epi);
+                    else epi.commit(ent_open, acc, pre_open);
                 }
                 acc = 0.0f;
             }
@@ -218,7 +232,7 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
 template <int KV, bool VALUED, bool SMEM, class X, class Epi>
 __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
                                        const float* wv, const X& x, Epi& epi, int lane) {
-    constexpr int UB = (VALUED ? 4 : 8) / KV;            // 4 (valued) / 8 (pattern) slots per lane in flight
+    constexpr int UB = ((VALUED ? TC_CM_SLOTS_V : TC_CM_SLOTS_P) + KV - 1) / KV;  // slots per lane in flight
     const int nk = d.w / KV;
     const int slabs = d.h >> 5;
     const int total = slabs * nk;
@@ -238,13 +252,16 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
                 if ((uu + 1) % nk == 0) ent[j] = __ldg(rid + 32 * (uu / nk));
             }
         }
+        typename Epi::Pre pre[UB];
+        #pragma unroll
+        for (int j = 0; j < UB; ++j) pre[j] = epi.prefetch(ent[j]);
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int uu = u0 + j;
             if (uu >= total) break;                      // warp-uniform
             acc += u[j].dot(x);
             if ((uu + 1) % nk == 0) {                    // row end (warp-uniform)
-                if (ent[j] != PAD_ROW) epi.write(ent[j], acc);
+                if (ent[j] != PAD_ROW) epi.commit(ent[j], acc, pre[j]);
                 acc = 0.0f;
             }
         }
@@ -417,19 +434,20 @@ __global__ void __launch_bounds__(kStreamThreads, 1) tc_spmv_wstream(TileArgs a,
 
 __host__ __device__ constexpr int ws_bar_bytes(int nwarps) { return ((2 * nwarps + 1) * 8 + 127) / 128 * 128; }
 
-// Epilogue interface: acc_in(ent) returns the partial sum of earlier tiles (0 unless FLAG_ACC),
-// put(ent, v) stores the row's (accumulated) value or applies the fused epilogue,
-// write(ent, v) = put(ent, v + acc_in(ent)).
+// Epilogue interface: prefetch(ent) loads what the row's write needs (the partial sum of earlier
+// tiles when FLAG_ACC, epilogue operands) early; commit(ent, v, pre) stores the row's value or
+// applies the fused epilogue; write(ent, v) = commit(ent, v, prefetch(ent)).
 // y = A x writer (no epilogue)
 struct EpiStore {
     float* y;
+    struct Pre { float acc; };
     __device__ __forceinline__ bool begin() { return true; }
     __device__ __forceinline__ void end() {}
-    __device__ __forceinline__ float acc_in(uint32_t ent) const {
-        return (ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f;
+    __device__ __forceinline__ Pre prefetch(uint32_t ent) const {
+        return Pre{(ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f};
     }
-    __device__ __forceinline__ void put(uint32_t ent, float v) { y[ent & ROW_MASK] = v; }
-    __device__ __forceinline__ void write(uint32_t ent, float v) { put(ent, v + acc_in(ent)); }
+    __device__ __forceinline__ void commit(uint32_t ent, float v, const Pre& pre) { y[ent & ROW_MASK] = v + pre.acc; }
+    __device__ __forceinline__ void write(uint32_t ent, float v) { commit(ent, v, prefetch(ent)); }
 };
 
 }  // namespace tc

@@ -296,7 +296,7 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
     bp.camping = opt.camping_pad != 0;
     bp.ell_h = opt.ell_h;
     PerfTable tab = table_for(opt.perf_table_path);
-    tab.max_act_warp = std::max(1, tab.max_act_warp / 148 * sm_count);
+    tab.max_act_warp = std::max(1, (int)((int64_t)tab.max_act_warp * sm_count / 148));
     if (opt.perf_table_path && !tab.loaded) { set_error("performance table unreadable"); return SPMV_ETABLE; }
     if (table_loaded) *table_loaded = tab.loaded ? 1 : 0;
 

@@ -1,0 +1,108 @@
+"""The product's performance model / auto-tuner against the oracle's transcription
+(oracle/model_ref.py) under a fixed offline table: per-tile predicted time equal to the
+transcription, and the auto-tuned WL the argmin of an independent re-enumeration (Alg. 2)."""
+import json
+import math
+
+import numpy as np
+import pytest
+
+import graphgen
+from oracle import format_ref, model_ref
+
+PERF = {"rm": 1.0e9, "cm": 2.5e9}          # constant per kind: lookup is exact, waves matter
+TABLE = dict(version=1, max_act_warp=96, launch_us=3.0, stage_GBps=5000.0, rmw_GBps=2500.0)
+
+
+def write_table(tmp_path):
+    ent = []
+    for cached in (0, 1):
+        for valued in (0, 1):
+            for w in (1, 8, 64, 4096):
+                for h in (1, 32, 1024):
+                    ent.append([cached, valued, 0, w, h, PERF["rm"]])
+                    ent.append([cached, valued, 1, w, h, PERF["cm"]])
+    path = tmp_path / "table.json"
+    path.write_text(json.dumps(dict(TABLE, entries=ent)))
+    return str(path)
+
+
+def tile_hists(n_rows, n_cols, rp, col, tw, T):
+    collen, perm, inv = format_ref.column_order(n_cols, col)
+    hists = [dict() for _ in range(T + 1)]
+    total = np.diff(rp)
+    for i in range(n_rows):
+        seg = np.zeros(T + 1, np.int64)
+        for k in inv[col[rp[i]:rp[i + 1]]]:
+            t = k // tw
+            seg[min(t, T)] += 1
+        for t in range(T + 1):
+            if seg[t] or (t == T and total[i] == 0):
+                hists[t][seg[t]] = hists[t].get(seg[t], 0) + 1
+    return [sorted(h.items(), key=lambda kv: -kv[0]) for h in hists]
+
+
+def expected_us(h, WL, t, T, tw, cached, split=True):
+    sec = model_ref.pm_packed(h, WL, lambda k, w, hh: PERF[k], TABLE["max_act_warp"], split=split)
+    rows = sum(c for _, c in h)
+    us = sec * 1e6
+    if rows:
+        us += TABLE["launch_us"]
+        if cached:
+            us += tw * 4.0 * 148 / (TABLE["stage_GBps"] * 1e3)
+        if t > 0:
+            us += rows * 8.0 / (TABLE["rmw_GBps"] * 1e3)
+    return us
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_predicted_time_equals_transcription(seed, tmp_path):
+    from paper_1103_2405_b200 import Plan
+    table = write_table(tmp_path)
+    rng = np.random.default_rng(seed)
+    nr, nc = int(rng.integers(200, 800)), int(rng.integers(200, 800))
+    rp, col, _ = graphgen.random_csr(nr, nc, int(rng.integers(2000, 20000)), seed=seed, kind="powerlaw", valued=False)
+    tw, T = 64, 3
+    wls = [int(x) for x in rng.choice([32, 64, 128, 256], size=T + 1)]
+    p = Plan(nr, nc, rp, col, None, device=-1, tile_width=tw, num_tiles=T, workload_sizes=wls,
+             perf_table_path=table)
+    st = p.stats()
+    assert st["perf_table_loaded"]
+    hists = tile_hists(nr, nc, rp, col, tw, T)
+    for t in range(T + 1):
+        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T)
+        assert math.isclose(st["tile_predicted_us"][t], exp, rel_tol=1e-9), (t, st["tile_predicted_us"][t], exp)
+
+
+def test_autotuned_wl_is_argmin(tmp_path):
+    """Alg. 2 (B200 candidates 128..4096): the chosen WL minimises the model (strict <, R22)."""
+    from paper_1103_2405_b200 import Plan
+    table = write_table(tmp_path)
+    G = graphgen.make_graph("t_small")
+    rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)
+    tw, T = 256, 2
+    p = Plan(G.n, G.n, rp, col, None, device=-1, tile_width=tw, num_tiles=T, perf_table_path=table)
+    st = p.stats()
+    hists = tile_hists(G.n, G.n, rp, col, tw, T)
+    for t in range(T + 1):
+        cands = [128, 256, 512, 1024, 2048, 4096]
+        times = [model_ref.pm_packed(hists[t], c, lambda k, w, h: PERF[k], TABLE["max_act_warp"]) for c in cands]
+        best = cands[int(np.argmin(times))]       # argmin keeps the first (smallest) on ties
+        assert st["wl"][t] == best, (t, st["wl"][t], best, times)
+
+
+def test_eq1_waves_in_product(tmp_path):
+    """2000 one-slot workloads with MAX_ACT_WARP = 960 form ceil(2000/960) = 3 waves (Eq. 1,
+    L124): with a uniform table the predicted time is the padded size, independent of waves."""
+    from paper_1103_2405_b200 import Plan
+    ent = [[c, v, k, w, h, 1e9] for c in (0, 1) for v in (0, 1) for k in (0, 1) for w in (1, 4096) for h in (1, 1024)]
+    path = tmp_path / "u.json"
+    path.write_text(json.dumps(dict(TABLE, max_act_warp=960, entries=ent)))
+    n = 2000
+    rp = np.arange(n + 1)
+    col = np.arange(n, dtype=np.int32)
+    p = Plan(n, n, rp, col, None, device=-1, tile_width=n, num_tiles=0, workload_sizes=[1],
+             align_rm=8, perf_table_path=str(path))
+    # WL=1, rows of length 1: w=1 >= hq=1 -> row major, padded to 8 slots; 2000 workloads
+    us = p.stats()["tile_predicted_us"][0]
+    assert math.isclose(us, 2000 * 8 / 1e9 * 1e6 + TABLE["launch_us"], rel_tol=1e-12)
