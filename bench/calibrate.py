@@ -28,13 +28,19 @@ N_UNCACHED = 4_847_571       # x of the LiveJournal-shaped config (L2-resident)
 TW_CACHED = 24576            # staged tile width (96 KB of x per CTA)
 
 
-def shape_matrix(kind, w, h, n_cols, target_slots, rng):
-    """rows of length w; WL = w*h makes every workload exactly (w, h)."""
+def shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw):
+    """rows of length w; WL = w*h makes every workload exactly (w, h).  Uncached tiles draw their
+    columns from a power law over the relabelled (hot-first) columns, as a power-law graph's
+    remainder does, so L1 reuse of hub columns is part of the measurement."""
     nw = max(1, target_slots // (w * h))
     n_rows = nw * h
-    col = rng.integers(0, n_cols, size=n_rows * w, dtype=np.int64)
-    # distinct columns inside a row keep the row length exactly w
-    if w > 1:
+    if powerlaw:
+        u = rng.random(n_rows * w)
+        col = np.minimum((n_cols * u ** 4.0).astype(np.int64), n_cols - 1)   # P(col < k) = (k/n)^(1/4): top 1% hold 32% (c2)
+    else:
+        col = rng.integers(0, n_cols, size=n_rows * w, dtype=np.int64)
+    # (duplicates inside a row are kept as separate entries by the builder, R9: rows stay w long)
+    if w > 1 and not powerlaw:
         col = col.reshape(n_rows, w)
         col = (col + np.arange(w)[None, :] * 7919) % n_cols
         col = col.reshape(-1)
@@ -45,7 +51,7 @@ def shape_matrix(kind, w, h, n_cols, target_slots, rng):
 def measure(kind, w, h, cached, valued, target_slots, reps=5):
     rng = np.random.default_rng(w * 1000 + h)
     n_cols = TW_CACHED if cached else N_UNCACHED
-    n_rows, rp, col = shape_matrix(kind, w, h, n_cols, target_slots, rng)
+    n_rows, rp, col = shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw=not cached)
     val = rng.uniform(0, 1, len(col)).astype(np.float32) if valued else None
     opt = dict(tile_width=TW_CACHED if cached else n_cols, num_tiles=1 if cached else 0,
                workload_size=w * h, align_rm=8)
@@ -70,11 +76,11 @@ def measure(kind, w, h, cached, valued, target_slots, reps=5):
 
 def main():
     quick = "--quick" in sys.argv
-    target = 4_000_000 if quick else 16_000_000
     rm_w = [8, 32, 128, 512, 2048] if quick else [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
-    rm_h = [1, 4, 16, 64] if quick else [1, 2, 4, 8, 16, 32, 64]
+    rm_h = [1, 4, 16, 32] if quick else [1, 2, 4, 8, 16, 32]
     cm_w = [1, 2, 4, 8, 16, 31] if quick else [1, 2, 3, 4, 6, 8, 12, 16, 24, 31]
-    cm_h = [32, 128, 512] if quick else [32, 64, 128, 256, 512, 1024]
+    cm_h = [32, 128, 512, 1024] if quick else [32, 64, 128, 256, 512, 1024]
+    resident = 148 * 32
     entries = []
     t0 = time.time()
     warps = 0
@@ -82,14 +88,16 @@ def main():
         for cached in (False, True):
             for w in rm_w:
                 for h in rm_h:
-                    if h > w or w * h > 32768:
+                    if h > w or w * h > 4096:
                         continue
+                    target = max(8_000_000, 2 * resident * w * h)   # >= 2 waves of workloads
                     sps, ms, warps = measure("rm", w, h, cached, valued, target)
                     entries.append([int(cached), int(valued), 0, w, h, round(sps, 1)])
             for w in cm_w:
                 for h in cm_h:
-                    if h <= w or w * h > 32768:
+                    if h <= w or w * h > 16384:
                         continue
+                    target = max(8_000_000, 2 * resident * w * h)
                     sps, ms, warps = measure("cm", w, h, cached, valued, target)
                     entries.append([int(cached), int(valued), 1, w, h, round(sps, 1)])
             print(f"valued={valued} cached={cached}: {len(entries)} entries, {time.time() - t0:.0f}s", flush=True)

@@ -129,6 +129,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
             (e = upload(&p->d_xp, xpz, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
+        if (const char* h = std::getenv("TCSPMV_L1_HOT")) p->l1_hot_cols = std::atoi(h);
         const char* kenv = std::getenv("TCSPMV_KERNEL");
         p->stream = kenv && std::string(kenv) == "stream";
         if (p->stream && (e = build_stream_tables(p))) {

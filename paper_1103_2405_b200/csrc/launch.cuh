@@ -36,6 +36,7 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
     a.desc = p.d_desc; a.wl_begin = ti.wl_begin; a.wl_end = ti.wl_end;
     a.col = p.d_col; a.val = p.d_val; a.row_id = p.d_row_id;
     a.x = xp + ti.col_lo; a.width = (int32_t)(ti.col_hi - ti.col_lo);
+    a.hot = p.l1_hot_cols;
     a.split = p.d_split; a.partials = p.d_partials; a.counters = p.d_counters;
     if (p.stream) {
         WsArgs s;

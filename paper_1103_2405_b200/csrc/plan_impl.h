@@ -37,6 +37,7 @@ struct spmv_plan_s {
     bool stream = true;
     int32_t stage_slots = 0;                  // slots per warp buffer (largest workload)
     int stream_grid = 0;
+    int32_t l1_hot_cols = 0x7fffffff;      // see TileArgs::hot (TCSPMV_L1_HOT overrides)
     int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
 };

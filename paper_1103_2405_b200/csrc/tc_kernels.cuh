@@ -42,6 +42,15 @@ namespace tc {
 #ifndef TC_CM_SLOTS_P
 #define TC_CM_SLOTS_P 2    // column major, pattern: slots per lane per batch
 #endif
+#ifndef TC_RM_UB_STAGED
+#define TC_RM_UB_STAGED 2
+#endif
+#ifndef TC_CM_SLOTS_V_STAGED
+#define TC_CM_SLOTS_V_STAGED 4
+#endif
+#ifndef TC_CM_SLOTS_P_STAGED
+#define TC_CM_SLOTS_P_STAGED 8
+#endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
 #endif
@@ -56,6 +65,8 @@ struct TileArgs {
     const uint32_t* row_id;
     const float* x;           // x' + col_lo: tile-relative base of the relabelled x
     int32_t width;            // tile width = padding sentinel
+    int32_t hot;              // unstaged tiles: columns below are gathered with L1 evict-last,
+                              // the rest evict-first (the relabelled hub columns stay in L1)
     const int32_t* split;     // [n_split][3]
     float* partials;          // [n_chunks]
     int32_t* counters;        // [n_split], zero between launches
@@ -90,13 +101,22 @@ template <bool SMEM> __device__ __forceinline__ float ld_f1(const float* p) {
 
 template <bool STAGED>
 struct XSrc {
+    // batch sizes (slots in flight per lane): shared-memory gathers are short-lived, so staged
+    // tiles afford deeper batches within the 64-register budget
+    static constexpr int kRmUnits = STAGED ? TC_RM_UB_STAGED : TC_RM_UB;
+    static constexpr int kCmSlotsV = STAGED ? TC_CM_SLOTS_V_STAGED : TC_CM_SLOTS_V;
+    static constexpr int kCmSlotsP = STAGED ? TC_CM_SLOTS_P_STAGED : TC_CM_SLOTS_P;
     const float* g;     // global base (tile-relative)
     const float* s;     // shared base
     int32_t width;
+    int32_t hot;
     __device__ __forceinline__ float operator()(int32_t c) const {
         if (c == width) return 0.0f;                  // padding slot (sentinel, reading R16)
         if (STAGED) return s[c];
-        return __ldg(g + c);
+        float v;
+        if (c < hot) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
+        else asm volatile("ld.global.nc.L1::evict_first.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
+        return v;
     }
 };
 
@@ -177,7 +197,7 @@ __device__ __forceinline__ void finish_split(const TileArgs& a, const WlDesc& d,
 template <bool VALUED, bool SMEM, class X, class Epi>
 __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
                                        const float* wv, const X& x, Epi& epi, int lane) {
-    constexpr int UB = TC_RM_UB;                         // int4 units per lane per batch
+    constexpr int UB = X::kRmUnits;                      // int4 units per lane per batch
     const int w4 = d.w >> 2;                             // int4 groups per row
     const int lpr = w4 >= 32 ? 32 : (w4 <= 1 ? 1 : (1 << (32 - __clz(w4 - 1))));
     const int lg = __ffs(lpr) - 1;
@@ -232,7 +252,7 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
 template <int KV, bool VALUED, bool SMEM, class X, class Epi>
 __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const int32_t* wc,
                                        const float* wv, const X& x, Epi& epi, int lane) {
-    constexpr int UB = ((VALUED ? TC_CM_SLOTS_V : TC_CM_SLOTS_P) + KV - 1) / KV;  // slots per lane in flight
+    constexpr int UB = ((VALUED ? X::kCmSlotsV : X::kCmSlotsP) + KV - 1) / KV;  // slots per lane in flight
     const int nk = d.w / KV;
     const int slabs = d.h >> 5;
     const int total = slabs * nk;
@@ -323,7 +343,7 @@ __device__ __forceinline__ void prefetch_workload(const TileArgs& a, int64_t j) 
 }
 
 template <bool STAGED, bool VALUED, class Epi>
-__global__ void __launch_bounds__(kThreads, TC_MINB) tc_spmv_tile(TileArgs a, Epi epi_in) {
+__global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(TileArgs a, Epi epi_in) {
     extern __shared__ float xs[];
     Epi epi = epi_in;
     if (!epi.begin()) return;                         // iteration loop already converged
@@ -343,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, TC_MINB) tc_spmv_tile(TileArgs a, Ep
         for (int i = h + 4 * n4 + threadIdx.x; i < n; i += kThreads) xs[i] = __ldg(src + i);
         __syncthreads();
     }
-    XSrc<STAGED> x{a.x, xs, a.width};
+    XSrc<STAGED> x{a.x, xs, a.width, a.hot};
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * kWarps;
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) tc_spmv_wstream(TileArgs a,
     WlDesc d = j < a.wl_end ? load_desc(a.desc + j) : WlDesc{};
     if (lane == 0 && j < a.wl_end) ws_issue<VALUED>(a, d, cbuf[0], vbuf[0], bars + 2 * warp, pol);
     if (STAGED) mbar_wait(xbar, 0);
-    XSrc<STAGED> x{a.x, xs, a.width};
+    XSrc<STAGED> x{a.x, xs, a.width, a.hot};
     for (int k = 0; j < a.wl_end; j += G, ++k) {
         const int cur = k & 1;
         const int64_t jn = j + G;

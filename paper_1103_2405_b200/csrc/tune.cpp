@@ -241,7 +241,7 @@ static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist,
     for (auto& h : hist) nnz += h.first * h.second;
     std::vector<int64_t> cand;
     if (bp.split) {
-        for (int64_t c = 128; c <= 4096; c *= 2) cand.push_back(c);
+        for (int64_t c = 256; c <= 1024; c *= 2) cand.push_back(c);   // range the calibration covers
     } else {
         const int64_t up = std::max<int64_t>(L, nnz / std::max(1, T.max_act_warp));
         for (int64_t c = L; c <= up && cand.size() < 64; c += L) cand.push_back(c);

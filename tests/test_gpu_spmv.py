@@ -104,3 +104,31 @@ def test_graph_auto_and_deterministic(gpu):
         check(a, rp, col, val, x)
         yh = p.execute_host(x)                       # host path through the C ABI
         assert yh.tobytes() == a.tobytes()
+
+
+def test_full_size_c2_sampled_rows(gpu):
+    """BASELINE configs[1] at full size, in the launch configuration bench.py times (auto plan,
+    valued): sampled rows (random + the 50 longest) against the oracle, one by one."""
+    import torch
+    from paper_1103_2405_b200 import Plan
+    G = graphgen.make_graph("c2")
+    val = graphgen.edge_values(G.keys, seed=graphgen.SEED_VAL, mode=1)
+    x = graphgen.uniform_f32(G.n, seed=graphgen.SEED_X)
+    p = Plan(G.n, G.n, G.row_ptr, G.col, val, device=0)
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.empty(G.n, device="cuda")
+    p.execute(xt, yt)
+    torch.cuda.synchronize()
+    y = yt.cpu().numpy()
+    lens = np.diff(G.row_ptr)
+    rows = np.unique(np.concatenate([np.random.default_rng(0).choice(G.n, 4000, replace=False),
+                                     np.argsort(lens)[-50:], np.nonzero(lens == 0)[0][:50]]))
+    sub_rp = np.concatenate([[0], np.cumsum(lens[rows])]).astype(np.int64)
+    idx = np.concatenate([np.arange(G.row_ptr[r], G.row_ptr[r + 1]) for r in rows])
+    yref, b = oracle.spmv(sub_rp, G.col[idx], val[idx], x)
+    err = np.abs(y[rows].astype(np.float64) - yref)
+    assert (err <= RTOL * b + 1e-30).all()
+    # bitwise deterministic at full size
+    y2 = torch.empty(G.n, device="cuda")
+    p.execute(xt, y2)
+    assert y2.cpu().numpy().tobytes() == y.tobytes()
