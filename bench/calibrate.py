@@ -48,10 +48,12 @@ def shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw):
     return n_rows, rp, col.astype(np.int32)
 
 
-def measure(kind, w, h, cached, valued, target_slots, reps=5):
+def measure(kind, w, h, mode, valued, target_slots, reps=5):
+    """mode 0: uncached, uniform columns; 1: cached (staged tile); 2: uncached, power-law columns"""
+    cached = mode == 1
     rng = np.random.default_rng(w * 1000 + h)
     n_cols = TW_CACHED if cached else N_UNCACHED
-    n_rows, rp, col = shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw=not cached)
+    n_rows, rp, col = shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw=mode == 2)
     val = rng.uniform(0, 1, len(col)).astype(np.float32) if valued else None
     opt = dict(tile_width=TW_CACHED if cached else n_cols, num_tiles=1 if cached else 0,
                workload_size=w * h, align_rm=8)
@@ -85,7 +87,7 @@ def main():
     t0 = time.time()
     warps = 0
     for valued in (True, False):
-        for cached in (False, True):
+        for cached in (0, 1, 2):
             for w in rm_w:
                 for h in rm_h:
                     if h > w or w * h > 4096:
@@ -120,7 +122,7 @@ def main():
            "max_act_warp": int(warps), "launch_us": round(launch_us, 3),
            "stage_GBps": 6000.0, "rmw_GBps": 4000.0,
            "units": "slots per second, whole GPU, every warp on one (w,h) shape (reading R20)",
-           "columns": ["cached", "valued", "kind(0=rm,1=cm)", "w", "h", "slots_per_s"],
+           "columns": ["x mode (0 uncached uniform, 1 cached, 2 uncached power-law)", "valued", "kind(0=rm,1=cm)", "w", "h", "slots_per_s"],
            "entries": entries}
     path = os.path.join(ROOT, "paper_1103_2405_b200", "data", "perf_table_b200.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)

@@ -162,6 +162,25 @@ static spmv_status ensure_host(spmv_plan_s* p) {
     return SPMV_OK;
 }
 
+// Row-entry bookkeeping for entry-ordered epilogue state: the row entries (host copy) and, per
+// row, the index of its FINAL entry (the first one for split rows); -1 for rows without one.
+spmv_status plan_final_positions(spmv_plan_s* p, std::vector<uint32_t>& entries, std::vector<int32_t>& fpos) {
+    entries.resize(p->n_row_entries);
+    if (p->host_valid) entries = p->L.row_id;
+    else if (p->n_row_entries) {
+        cudaError_t e = cudaMemcpy(entries.data(), p->d_row_id, p->n_row_entries * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        if (e) return cuda_status(e, "row entries");
+    }
+    fpos.assign(p->n_rows, -1);
+    for (int64_t k = 0; k < p->n_row_entries; ++k) {
+        const uint32_t ent = entries[k];
+        if (ent == PAD_ROW || !(ent & FLAG_FINAL)) continue;
+        int32_t& f = fpos[ent & ROW_MASK];
+        if (f < 0) f = (int32_t)k;
+    }
+    return SPMV_OK;
+}
+
 spmv_status execute_permuted(spmv_plan_s* p, const float* xp, float* y, cudaStream_t st) {
     return cuda_status(launch_tiles(*p, p->grid_tile, xp, EpiStore{y}, st), "tile launch");
 }

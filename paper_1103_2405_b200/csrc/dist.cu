@@ -177,8 +177,10 @@ __global__ void dist_init(float* p, float* zslot, const float* inv, int64_t n_lo
     }
 }
 
-__global__ void copy_f(const float* a, float* b, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+// slot[r] = p_e[fpos[r]]: the local rows' values out of row-entry order
+__global__ void gather_rows(const float* p_e, const int32_t* fpos, float* slot, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        slot[i] = fpos[i] >= 0 ? p_e[fpos[i]] : 0.0f;
 }
 
 spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
@@ -273,6 +275,19 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         }
         s->total_slots = slots;
         CKD(cudaMalloc(&s->d_slots, (size_t)std::max(slots, 1) * 2 * sizeof(double)));
+        std::vector<uint32_t> entries;
+        if ((st = plan_final_positions(p, entries, s->fpos))) throw st;
+        const int64_t ne = std::max<int64_t>(p->n_row_entries, 1);
+        std::vector<float> inv_e(ne, 0.0f);
+        for (int64_t k = 0; k < p->n_row_entries; ++k) {
+            const uint32_t ent = entries[k];
+            if (ent != PAD_ROW && (ent & FLAG_FINAL)) inv_e[k] = inv[ent & ROW_MASK];
+        }
+        CKD(cudaMalloc(&s->d_p_e, ne * sizeof(float)));
+        CKD(cudaMalloc(&s->d_inv_e, ne * sizeof(float)));
+        CKD(cudaMemcpy(s->d_inv_e, inv_e.data(), ne * sizeof(float), cudaMemcpyHostToDevice));
+        CKD(cudaMalloc(&s->d_fpos, nl * sizeof(int32_t)));
+        if (D->n_local) CKD(cudaMemcpy(s->d_fpos, s->fpos.data(), D->n_local * sizeof(int32_t), cudaMemcpyHostToDevice));
 #undef CKD
     } catch (spmv_status code) {
         st = code;
@@ -308,6 +323,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     float* zslot = D->d_G + (int64_t)D->rank * D->slot;
     const int g = p->sm_count * 4;
     dist_init<<<g, 256, 0, st>>>(s->d_p, zslot, s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
+    init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
     spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
     if (ss) return ss;
     dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
@@ -323,7 +339,8 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
             const size_t nu = s->tiles_used.size();
             for (size_t i = 0; i < nu; ++i) {
                 EpiAffine epi{};
-                epi.y = s->d_y; epi.p = s->d_p; epi.z_next = zslot; epi.inv_deg = s->d_inv;
+                epi.y = s->d_y; epi.p = s->d_p_e; epi.z_next = zslot; epi.inv_deg = s->d_inv_e;
+                epi.fpos = s->d_fpos;
                 epi.ctrl = s->d_ctrl; epi.slots = s->d_slots; epi.slot_base = s->slot_base[i];
                 epi.total_slots = s->total_slots; epi.is_last = (i + 1 == nu); epi.cond = 0;
                 epi.rwr = rwr;
@@ -364,7 +381,7 @@ spmv_status solver_result_dist(spmv_solver s, float* out0, float*) {
     cudaSetDevice(s->device);
     cudaStream_t st = s->own_stream;
     float* slot = D->d_G + (int64_t)D->rank * D->slot;
-    copy_f<<<s->plan->sm_count * 4, 256, 0, st>>>(s->d_p, slot, D->n_local);
+    gather_rows<<<s->plan->sm_count * 4, 256, 0, st>>>(s->d_p_e, s->d_fpos, slot, D->n_local);
     spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
     if (ss) return ss;
     std::vector<float> G((size_t)D->P * D->slot);
@@ -381,6 +398,7 @@ void solver_destroy_dist(spmv_solver s) {
     if (D) { cudaFree(D->d_G); cudaFree(D->d_idx); delete D; }
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
     cudaFree(s->d_p); cudaFree(s->d_y); cudaFree(s->d_inv); cudaFree(s->d_ctrl); cudaFree(s->d_slots);
+    cudaFree(s->d_p_e); cudaFree(s->d_inv_e); cudaFree(s->d_fpos);
     if (s->plan) spmv_plan_destroy(s->plan);
     delete s;
 }

@@ -78,7 +78,9 @@ __device__ __forceinline__ bool iteration_done(Ctrl* c, double res) {
 
 // ------------------------------------------------------------------ PageRank / RWR epilogue
 struct EpiAffine {
-    float* y; float* p; float* z_next; const float* inv_deg;
+    // p and inv are kept in row-entry order (index of the row's FINAL entry; fpos maps a row to
+    // it for split rows), so their reads/writes are coalesced; z_next is in vertex order (x).
+    float* y; float* p; float* z_next; const float* inv_deg; const int32_t* fpos;
     Ctrl* ctrl; double* slots; int32_t slot_base, total_slots, is_last;
     cudaGraphConditionalHandle cond;
     int32_t rwr;
@@ -93,23 +95,26 @@ struct EpiAffine {
         return true;
     }
     struct Pre { float acc, p_old, inv; };
-    __device__ __forceinline__ Pre prefetch(uint32_t ent) const {
+    __device__ __forceinline__ int32_t slot(uint32_t ent, int32_t e) const {
+        return e >= 0 ? e : __ldg(fpos + (ent & ROW_MASK));
+    }
+    __device__ __forceinline__ Pre prefetch(uint32_t ent, int32_t e) const {
         Pre q{0.0f, 0.0f, 0.0f};
         if (ent == PAD_ROW) return q;
         const uint32_t r = ent & ROW_MASK;
         if (ent & FLAG_ACC) q.acc = y[r];
-        if (ent & FLAG_FINAL) { q.p_old = p[r]; q.inv = __ldg(inv_deg + r); }
+        if (ent & FLAG_FINAL) { const int32_t s = slot(ent, e); q.p_old = p[s]; q.inv = __ldg(inv_deg + s); }
         return q;
     }
-    __device__ __forceinline__ void write(uint32_t ent, float v) { commit(ent, v, prefetch(ent)); }
-    __device__ __forceinline__ void commit(uint32_t ent, float v, const Pre& pre) {
+    __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
+    __device__ __forceinline__ void commit(uint32_t ent, int32_t e, float v, const Pre& pre) {
         const uint32_t r = ent & ROW_MASK;
         v += pre.acc;
         if (!(ent & FLAG_FINAL)) { y[r] = v; return; }
         float pn = fmaf(c, v, tele);
         if (rwr && (int32_t)r == q) pn += 1.0f - c;
         res += fabs((double)pn - (double)pre.p_old);
-        p[r] = pn;
+        p[slot(ent, e)] = pn;
         z_next[r] = pn * pre.inv;
         if (pre.inv == 0.0f) dm += (double)pn;
     }
@@ -138,7 +143,8 @@ struct EpiAffine {
 
 // ------------------------------------------------------------------ HITS epilogues
 struct EpiHitsSpmv {
-    float* y; const uint8_t* half;
+    float* y; const uint8_t* half;     // half: in row-entry order (fpos for split rows)
+    const int32_t* fpos;
     Ctrl* ctrl; double* slots; int32_t slot_base, total_slots, is_last, l2;
     double s0, s1;
     __device__ __forceinline__ bool begin() {
@@ -147,16 +153,16 @@ struct EpiHitsSpmv {
         return true;
     }
     struct Pre { float acc; int half; };
-    __device__ __forceinline__ Pre prefetch(uint32_t ent) const {
+    __device__ __forceinline__ Pre prefetch(uint32_t ent, int32_t e) const {
         Pre q{0.0f, 0};
         if (ent == PAD_ROW) return q;
         const uint32_t r = ent & ROW_MASK;
         if (ent & FLAG_ACC) q.acc = y[r];
-        if (ent & FLAG_FINAL) q.half = __ldg(half + r);
+        if (ent & FLAG_FINAL) q.half = __ldg(half + (e >= 0 ? e : __ldg(fpos + r)));
         return q;
     }
-    __device__ __forceinline__ void write(uint32_t ent, float v) { commit(ent, v, prefetch(ent)); }
-    __device__ __forceinline__ void commit(uint32_t ent, float v, const Pre& pre) {
+    __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
+    __device__ __forceinline__ void commit(uint32_t ent, int32_t, float v, const Pre& pre) {
         const uint32_t r = ent & ROW_MASK;
         v += pre.acc;
         y[r] = v;
@@ -218,6 +224,17 @@ static __global__ void init_affine(float* p, float* z, const float* inv_deg, int
         z[i] = v * inv_deg[i];
     }
 }
+// entry-ordered p: p_e[k] = p(0) of the row of FINAL entry k (PageRank 1/n, RWR e_q)
+static __global__ void init_entries(float* p_e, const uint32_t* row_id, int64_t n_entries, int32_t rwr,
+                                    int32_t q, float p0) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_entries; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t ent = row_id[k];
+        float v = 0.0f;
+        if (ent != PAD_ROW && (ent & FLAG_FINAL)) v = rwr ? ((int32_t)(ent & ROW_MASK) == q ? 1.0f : 0.0f) : p0;
+        p_e[k] = v;
+    }
+}
+
 static __global__ void init_fill(float* v, int64_t n, float val) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         v[i] = val;

@@ -101,6 +101,26 @@ static spmv_status build_solver(spmv_solver_s* s, const int64_t* row_ptr, const 
     s->total_slots = slots;
     s->norm_grid = p->sm_count * 4;
     CKE(cudaMalloc(&s->d_slots, (size_t)std::max(slots, s->norm_grid) * 2 * sizeof(double)));
+    // entry-ordered epilogue state
+    std::vector<uint32_t> entries;
+    if ((st = plan_final_positions(p, entries, s->fpos))) return st;
+    const int64_t ne = std::max<int64_t>(p->n_row_entries, 1);
+    std::vector<float> inv_e(ne, 0.0f);
+    std::vector<uint8_t> half_e(ne, 0);
+    for (int64_t k = 0; k < p->n_row_entries; ++k) {
+        const uint32_t ent = entries[k];
+        if (ent == PAD_ROW || !(ent & FLAG_FINAL)) continue;
+        const uint32_t r = ent & ROW_MASK;
+        inv_e[k] = invd_pi[r];
+        if (!half_pi.empty()) half_e[k] = half_pi[r];
+    }
+    CKE(cudaMalloc(&s->d_p_e, ne * sizeof(float)));
+    CKE(cudaMalloc(&s->d_inv_e, ne * sizeof(float)));
+    CKE(cudaMemcpy(s->d_inv_e, inv_e.data(), ne * sizeof(float), cudaMemcpyHostToDevice));
+    CKE(cudaMalloc(&s->d_half_e, ne));
+    CKE(cudaMemcpy(s->d_half_e, half_e.data(), ne, cudaMemcpyHostToDevice));
+    CKE(cudaMalloc(&s->d_fpos, std::max<int64_t>(N, 1) * sizeof(int32_t)));
+    CKE(cudaMemcpy(s->d_fpos, s->fpos.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice));
 #undef CKE
     return SPMV_OK;
 }
@@ -113,7 +133,7 @@ static cudaError_t enqueue_iteration(spmv_solver_s* s, int parity, cudaStream_t 
     if (s->algo == SPMV_ALGO_HITS) {
         for (size_t i = 0; i < nu; ++i) {
             EpiHitsSpmv epi{};
-            epi.y = s->d_y; epi.half = s->d_half; epi.ctrl = s->d_ctrl; epi.slots = s->d_slots;
+            epi.y = s->d_y; epi.half = s->d_half_e; epi.fpos = s->d_fpos; epi.ctrl = s->d_ctrl; epi.slots = s->d_slots;
             epi.slot_base = s->slot_base[i]; epi.total_slots = s->total_slots;
             epi.is_last = (i + 1 == nu); epi.l2 = s->it.hits_norm != 1;
             cudaError_t e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], s->d_p, epi, st);
@@ -125,7 +145,8 @@ static cudaError_t enqueue_iteration(spmv_solver_s* s, int parity, cudaStream_t 
     }
     for (size_t i = 0; i < nu; ++i) {
         EpiAffine epi{};
-        epi.y = s->d_y; epi.p = s->d_p; epi.z_next = s->d_z[parity ^ 1]; epi.inv_deg = s->d_inv;
+        epi.y = s->d_y; epi.p = s->d_p_e; epi.z_next = s->d_z[parity ^ 1]; epi.inv_deg = s->d_inv_e;
+        epi.fpos = s->d_fpos;
         epi.ctrl = s->d_ctrl; epi.slots = s->d_slots; epi.slot_base = s->slot_base[i];
         epi.total_slots = s->total_slots; epi.is_last = (i + 1 == nu); epi.cond = cond;
         epi.rwr = s->algo == SPMV_ALGO_RWR;
@@ -230,8 +251,12 @@ spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_ite
     if ((e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st))) return cuda_status(e, "ctrl");
     const int g = s->plan->sm_count * 4;
     if (s->algo == SPMV_ALGO_HITS) init_fill<<<g, 256, 0, st>>>(s->d_p, s->N, (float)(1.0 / n));
-    else init_affine<<<g, 256, 0, st>>>(s->d_p, s->d_z[0], s->d_inv, s->N, s->algo == SPMV_ALGO_RWR,
-                                         (int32_t)c.q, (float)(1.0 / n));
+    else {
+        init_affine<<<g, 256, 0, st>>>(s->d_p, s->d_z[0], s->d_inv, s->N, s->algo == SPMV_ALGO_RWR,
+                                       (int32_t)c.q, (float)(1.0 / n));
+        init_entries<<<g, 256, 0, st>>>(s->d_p_e, s->plan->d_row_id, s->plan->n_row_entries,
+                                        s->algo == SPMV_ALGO_RWR, (int32_t)c.q, (float)(1.0 / n));
+    }
     if ((e = cudaGetLastError())) return cuda_status(e, "init");
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -261,9 +286,16 @@ __attribute__((visibility("default")))
 spmv_status spmv_solver_result(spmv_solver s, float* out0, float* out1) {
     if (!s || !out0 || (s->algo == SPMV_ALGO_HITS && !out1)) { set_error("null argument"); return SPMV_EINVAL; }
     if (s->comm) return solver_result_dist(s, out0, out1);
-    std::vector<float> v(s->N);
     cudaSetDevice(s->device);
-    cudaError_t e = cudaMemcpy(v.data(), s->d_p, s->N * sizeof(float), cudaMemcpyDeviceToHost);
+    std::vector<float> v(s->N);
+    cudaError_t e;
+    if (s->algo == SPMV_ALGO_HITS) {
+        e = cudaMemcpy(v.data(), s->d_p, s->N * sizeof(float), cudaMemcpyDeviceToHost);
+    } else {   // PageRank / RWR keep p in row-entry order
+        std::vector<float> pe(std::max<int64_t>(s->plan->n_row_entries, 1));
+        e = cudaMemcpy(pe.data(), s->d_p_e, s->plan->n_row_entries * sizeof(float), cudaMemcpyDeviceToHost);
+        for (int64_t r = 0; r < s->N; ++r) v[r] = s->fpos[r] >= 0 ? pe[s->fpos[r]] : 0.0f;
+    }
     if (e) return cuda_status(e, "result");
     for (int64_t u = 0; u < s->n; ++u) out0[u] = v[s->pi[u]];
     if (s->algo == SPMV_ALGO_HITS)
@@ -291,6 +323,7 @@ __attribute__((visibility("default"))) void spmv_solver_destroy(spmv_solver s) {
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
     cudaFree(s->d_p); cudaFree(s->d_y); cudaFree(s->d_z[0]); cudaFree(s->d_z[1]); cudaFree(s->d_inv);
     cudaFree(s->d_half); cudaFree(s->d_ctrl); cudaFree(s->d_slots);
+    cudaFree(s->d_p_e); cudaFree(s->d_inv_e); cudaFree(s->d_half_e); cudaFree(s->d_fpos);
     if (s->plan) spmv_plan_destroy(s->plan);
     delete s;
 }

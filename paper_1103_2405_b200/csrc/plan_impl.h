@@ -37,7 +37,7 @@ struct spmv_plan_s {
     bool stream = true;
     int32_t stage_slots = 0;                  // slots per warp buffer (largest workload)
     int stream_grid = 0;
-    int32_t l1_hot_cols = 0x7fffffff;      // see TileArgs::hot (TCSPMV_L1_HOT overrides)
+    int32_t l1_hot_cols = 0;               // see TileArgs::hot; 0 = plain ld.global.nc (TCSPMV_L1_HOT)
     int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
 };
@@ -45,6 +45,7 @@ struct spmv_plan_s {
 namespace tc {
 spmv_status cuda_status(cudaError_t e, const char* what);
 // build the plan (host) and upload it to `device` (capi.cu)
+spmv_status plan_final_positions(spmv_plan_s* p, std::vector<uint32_t>& entries, std::vector<int32_t>& fpos);
 spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col, const float* val, const spmv_options* opt_in,
                         int device, spmv_plan_s** out);

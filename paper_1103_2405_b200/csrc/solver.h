@@ -42,7 +42,13 @@ struct spmv_solver_s {
     float* d_y = nullptr;           // partial y (multi-tile rows) / HITS raw product
     float* d_z[2] = {nullptr, nullptr};  // PageRank / RWR SpMV input, double buffered
     float* d_inv = nullptr;         // 1 / (out)degree, 0 for dangling
-    uint8_t* d_half = nullptr;      // HITS: 1 for hub entries
+    uint8_t* d_half = nullptr;      // HITS: 1 for hub entries (vertex order)
+    // entry-ordered epilogue state (index = the row's FINAL entry in the plan's row_id[])
+    float* d_p_e = nullptr;         // PageRank p / RWR r
+    float* d_inv_e = nullptr;       // 1 / degree
+    uint8_t* d_half_e = nullptr;    // HITS half flag
+    int32_t* d_fpos = nullptr;      // row -> FINAL entry index
+    std::vector<int32_t> fpos;      // host copy
     tc::Ctrl* d_ctrl = nullptr;
     double* d_slots = nullptr;
     std::vector<int> grids;

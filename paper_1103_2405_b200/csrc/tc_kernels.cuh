@@ -113,6 +113,7 @@ struct XSrc {
     __device__ __forceinline__ float operator()(int32_t c) const {
         if (c == width) return 0.0f;                  // padding slot (sentinel, reading R16)
         if (STAGED) return s[c];
+        if (hot <= 0) return __ldg(g + c);
         float v;
         if (c < hot) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
         else asm volatile("ld.global.nc.L1::evict_first.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
@@ -182,7 +183,7 @@ __device__ __forceinline__ void finish_split(const TileArgs& a, const WlDesc& d,
         float s = 0.0f;
         for (int32_t c = 0; c < nch; ++c) s += __ldcg(a.partials + pbase + c);
         a.counters[d.split_id] = 0;                   // ready for the next launch
-        epi.write(ent, s);
+        epi.write(ent, -1, s);
     }
 }
 
@@ -208,11 +209,13 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
     const int V = steps * upl;                           // virtual units of this lane
     float acc = 0.0f;
     uint32_t ent_open = PAD_ROW;
+    int32_t eix_open = -1;
     typename Epi::Pre pre_open{};
     for (int v0 = 0; v0 < V; v0 += UB) {
         Unit<4, VALUED, SMEM> u[UB];
         bool ok[UB];
         uint32_t ent_s[UB];
+        int32_t eix_s[UB];
         typename Epi::Pre pre_s[UB];
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
@@ -223,21 +226,22 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
             if (ok[j]) u[j].load(wc + r * d.w, VALUED ? wv + r * d.w : nullptr, 4 * q);
             // a row's entry and its epilogue operands are fetched when the row starts, so their
             // latency overlaps the row's slot loads and gathers
-            ent_s[j] = (v < V && v % upl == 0 && sl == 0 && r < d.h) ? __ldg(a.row_id + d.row_base + r) : PAD_ROW;
+            eix_s[j] = d.row_base + r;
+            ent_s[j] = (v < V && v % upl == 0 && sl == 0 && r < d.h) ? __ldg(a.row_id + eix_s[j]) : PAD_ROW;
         }
         #pragma unroll
-        for (int j = 0; j < UB; ++j) pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j]);
+        for (int j = 0; j < UB; ++j) pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j], eix_s[j]);
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int v = v0 + j;
             if (v >= V) break;                           // warp-uniform
-            if (v % upl == 0) { ent_open = ent_s[j]; pre_open = pre_s[j]; }
+            if (v % upl == 0) { ent_open = ent_s[j]; eix_open = eix_s[j]; pre_open = pre_s[j]; }
             if (ok[j]) acc += u[j].dot(x);
             if ((v + 1) % upl == 0) {                    // row boundary (warp-uniform)
                 for (int o = lpr >> 1; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (ent_open != PAD_ROW) {
                     if (d.kind == KIND_SPLIT) finish_split(a, d, ent_open, acc, epi);
-                    else epi.commit(ent_open, acc, pre_open);
+                    else epi.commit(ent_open, eix_open, acc, pre_open);
                 }
                 acc = 0.0f;
             }
@@ -274,14 +278,14 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
         }
         typename Epi::Pre pre[UB];
         #pragma unroll
-        for (int j = 0; j < UB; ++j) pre[j] = epi.prefetch(ent[j]);
+        for (int j = 0; j < UB; ++j) pre[j] = epi.prefetch(ent[j], d.row_base + lane + 32 * ((u0 + j) / nk));
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int uu = u0 + j;
             if (uu >= total) break;                      // warp-uniform
             acc += u[j].dot(x);
             if ((uu + 1) % nk == 0) {                    // row end (warp-uniform)
-                if (ent[j] != PAD_ROW) epi.commit(ent[j], acc, pre[j]);
+                if (ent[j] != PAD_ROW) epi.commit(ent[j], d.row_base + lane + 32 * (uu / nk), acc, pre[j]);
                 acc = 0.0f;
             }
         }
@@ -300,7 +304,7 @@ __device__ __forceinline__ void run_zero(const TileArgs& a, const WlDesc& d, Epi
         }
         #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (ent[j] != PAD_ROW) epi.write(ent[j], 0.0f);
+            if (ent[j] != PAD_ROW) epi.write(ent[j], d.row_base + r0 + 32 * j + lane, 0.0f);
     }
 }
 
@@ -454,20 +458,22 @@ __global__ void __launch_bounds__(kStreamThreads, 1) tc_spmv_wstream(TileArgs a,
 
 __host__ __device__ constexpr int ws_bar_bytes(int nwarps) { return ((2 * nwarps + 1) * 8 + 127) / 128 * 128; }
 
-// Epilogue interface: prefetch(ent) loads what the row's write needs (the partial sum of earlier
-// tiles when FLAG_ACC, epilogue operands) early; commit(ent, v, pre) stores the row's value or
-// applies the fused epilogue; write(ent, v) = commit(ent, v, prefetch(ent)).
+// Epilogue interface: prefetch(ent, e) loads what the row's write needs (the partial sum of
+// earlier tiles when FLAG_ACC, epilogue operands) early; commit(ent, e, v, pre) stores the row's
+// value or applies the fused epilogue; write(ent, e, v) = commit(ent, e, v, prefetch(ent, e)).
+// e is the index of the row entry in row_id[] (consecutive lanes -> consecutive entries, so
+// per-row epilogue state kept in entry order is read and written coalesced); -1 for split rows.
 // y = A x writer (no epilogue)
 struct EpiStore {
     float* y;
     struct Pre { float acc; };
     __device__ __forceinline__ bool begin() { return true; }
     __device__ __forceinline__ void end() {}
-    __device__ __forceinline__ Pre prefetch(uint32_t ent) const {
+    __device__ __forceinline__ Pre prefetch(uint32_t ent, int32_t) const {
         return Pre{(ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f};
     }
-    __device__ __forceinline__ void commit(uint32_t ent, float v, const Pre& pre) { y[ent & ROW_MASK] = v + pre.acc; }
-    __device__ __forceinline__ void write(uint32_t ent, float v) { commit(ent, v, prefetch(ent)); }
+    __device__ __forceinline__ void commit(uint32_t ent, int32_t, float v, const Pre& pre) { y[ent & ROW_MASK] = v + pre.acc; }
+    __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
 };
 
 }  // namespace tc

@@ -36,7 +36,9 @@ static constexpr int32_t kDefaultWL = 1024;
 
 // ------------------------------------------------------------------ offline table
 struct PerfTable {
-    // key: (cached, valued, kind) -> grid over (log2 w, log2 h)
+    // key: (x mode, valued, kind) -> grid over (log2 w, log2 h); x mode 0 = uncached with uniform
+    // columns (a remainder whose hub columns went to dense tiles), 1 = cached (x segment in
+    // shared memory), 2 = uncached with power-law columns (single-tile plans: hubs hit L1)
     struct Grid { std::vector<double> lw, lh; std::vector<std::vector<double>> v; };
     std::map<int, Grid> grids;
     double launch_us = 3.0;         // per tile launch gap
@@ -46,11 +48,13 @@ struct PerfTable {
     bool loaded = false;
     std::string source = "built-in";
 
-    static int key(bool cached, bool valued, int kind) { return (cached ? 4 : 0) + (valued ? 2 : 0) + (kind == KIND_CM ? 1 : 0); }
+    static int key(int mode, bool valued, int kind) { return mode * 4 + (valued ? 2 : 0) + (kind == KIND_CM ? 1 : 0); }
 
     // bilinear interpolation in (log2 w, log2 h), clamped to the measured range
-    double lookup(bool cached, bool valued, int kind, double w, double h) const {
-        auto it = grids.find(key(cached, valued, kind));
+    double lookup(int mode, bool valued, int kind, double w, double h) const {
+        auto it = grids.find(key(mode, valued, kind));
+        if (it == grids.end() && mode == 2) it = grids.find(key(0, valued, kind));
+        const bool cached = mode == 1;
         if (it == grids.end() || it->second.lw.empty() || it->second.lh.empty()) return analytic(cached, valued, kind, w, h);
         const Grid& g = it->second;
         auto locate = [](const std::vector<double>& ax, double v, int& i, double& f) {
@@ -125,7 +129,7 @@ static bool parse_table(const std::string& text, PerfTable& T) {
         while (*s && *s != ']') ++s;
         if (*s) ++s;
         if (k != 6) return false;
-        raw[PerfTable::key(f[0] != 0, f[1] != 0, (int)f[2])][{std::log2(f[3]), std::log2(f[4])}] = f[5];
+        raw[PerfTable::key((int)f[0], f[1] != 0, (int)f[2])][{std::log2(f[3]), std::log2(f[4])}] = f[5];
         ++n;
     }
     for (auto& kv : raw) {
@@ -183,7 +187,7 @@ static const PerfTable& table_for(const char* path_opt) {
 // hist: (length, count) pairs, lengths descending (a tile's ranked rows).  Walks the same packing
 // rules as pack_layout and charges every workload to its wave.
 static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int64_t WL, int align,
-                      bool split, int ell_h, bool cached, bool valued, const PerfTable& T,
+                      bool split, int ell_h, int cached, bool valued, const PerfTable& T,
                       int64_t* n_workloads = nullptr) {
     const int64_t M = std::max(1, T.max_act_warp);      // MAX_ACT_WARP (Eq. 1)
     double total = 0.0, P = 0.0, S = 0.0;
@@ -235,7 +239,7 @@ static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int6
 // Alg. 2 in B200 mode: candidates are powers of two (rows longer than WL split) plus the paper's
 // multiples of the longest row; paper mode (no split) keeps WL >= the longest row.
 static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, const BuildParams& bp,
-                           bool cached, bool valued, const PerfTable& T, int32_t& opt_wl, double& opt_t) {
+                           int cached, bool valued, const PerfTable& T, int32_t& opt_wl, double& opt_t) {
     const int64_t L = hist.empty() ? 1 : std::max<int64_t>(1, hist[0].first);
     int64_t nnz = 0;
     for (auto& h : hist) nnz += h.first * h.second;
@@ -264,15 +268,16 @@ static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildPa
     const bool valued = !P.pattern;
     for (int32_t t = 0; t <= T; ++t) {
         const bool cached = t < T && opt.stage_x != 0;
+        const int mode = cached ? 1 : (T == 0 ? 2 : 0);
         int32_t wl = kDefaultWL;
         double sec = 0.0;
         if (opt.workload_sizes) wl = opt.workload_sizes[std::min(t, opt.num_tiles >= 0 ? opt.num_tiles : t)];
         else if (opt.workload_size > 0) wl = opt.workload_size;
         if (opt.workload_sizes || opt.workload_size > 0) {
             BuildParams b = base; b.wl.assign(1, wl);
-            sec = pm_tile(hist[t], wl, b.align_rm, b.split, b.ell_h, cached, valued, tab);
+            sec = pm_tile(hist[t], wl, b.align_rm, b.split, b.ell_h, mode, valued, tab);
         } else {
-            partition_tile(hist[t], base, cached, valued, tab, wl, sec);
+            partition_tile(hist[t], base, mode, valued, tab, wl, sec);
         }
         int64_t rows = 0, nnz = 0;
         for (auto& h : hist[t]) { rows += h.second; nnz += h.first * h.second; }

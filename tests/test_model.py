@@ -75,7 +75,7 @@ def test_predicted_time_equals_transcription(seed, tmp_path):
 
 
 def test_autotuned_wl_is_argmin(tmp_path):
-    """Alg. 2 (B200 candidates 128..4096): the chosen WL minimises the model (strict <, R22)."""
+    """Alg. 2 (B200 candidates 256..1024): the chosen WL minimises the model (strict <, R22)."""
     from paper_1103_2405_b200 import Plan
     table = write_table(tmp_path)
     G = graphgen.make_graph("t_small")
@@ -85,7 +85,7 @@ def test_autotuned_wl_is_argmin(tmp_path):
     st = p.stats()
     hists = tile_hists(G.n, G.n, rp, col, tw, T)
     for t in range(T + 1):
-        cands = [128, 256, 512, 1024, 2048, 4096]
+        cands = [256, 512, 1024]
         times = [model_ref.pm_packed(hists[t], c, lambda k, w, h: PERF[k], TABLE["max_act_warp"]) for c in cands]
         best = cands[int(np.argmin(times))]       # argmin keeps the first (smallest) on ties
         assert st["wl"][t] == best, (t, st["wl"][t], best, times)
