@@ -169,7 +169,9 @@ typedef struct {
  * times; `comm` = NULL runs on one GPU, else the row-partitioned multi-GPU path (Sec. 3.2):
  * every rank passes the whole graph, owns the rows bitonic_partition gives it, runs its local
  * tiled-composite SpMV with the fused epilogue, and the next x plus the fp64 partials are
- * exchanged by one NCCL allgather per iteration (PageRank and RWR; HITS returns SPMV_EINVAL). */
+ * exchanged by one NCCL allgather per iteration.  HITS exchanges the raw product with its half
+ * sums and normalises after the exchange; its stop decision lags one SpMV (the converged iterate
+ * is the one returned). */
 spmv_status spmv_solver_create(int algo, int64_t n, int64_t m, const int64_t* row_ptr,
                                const int32_t* col, const spmv_iter_opts* it,
                                const spmv_options* opt, spmv_comm comm, int device,

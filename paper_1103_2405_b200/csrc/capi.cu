@@ -52,7 +52,7 @@ static void free_device(spmv_plan_s* p) {
     cudaSetDevice(p->device);
     cudaFree(p->d_desc); cudaFree(p->d_row_id); cudaFree(p->d_col); cudaFree(p->d_val);
     cudaFree(p->d_perm); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
-    cudaFree(p->d_counters);
+    cudaFree(p->d_counters); cudaFree(p->d_hx);
     cudaSetDevice(cur);
 }
 
@@ -130,6 +130,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
         if (const char* h = std::getenv("TCSPMV_L1_HOT")) p->l1_hot_cols = std::atoi(h);
+        if (const char* h = std::getenv("TCSPMV_PREFIX")) p->x_prefix = std::atoi(h) / 4 * 4;
         const char* kenv = std::getenv("TCSPMV_KERNEL");
         p->stream = kenv && std::string(kenv) == "stream";
         if (p->stream && (e = build_stream_tables(p))) {
@@ -251,15 +252,15 @@ spmv_status spmv_execute_host(spmv_plan p, const float* xh, float* yh, void* str
     cudaError_t e = cudaSetDevice(p->device);
     if (e) return cuda_status(e, "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
-    float *dx = nullptr, *dy = nullptr;
-    if ((e = cudaMallocAsync(&dx, std::max<int64_t>(p->n_cols, 1) * 4, st)) ||
-        (e = cudaMallocAsync(&dy, std::max<int64_t>(p->n_rows, 1) * 4, st)))
-        return cuda_status(e, "cudaMallocAsync");
+    // device staging buffers owned by the plan (allocated on first use)
+    if (!p->d_hx && (e = cudaMalloc(&p->d_hx, std::max<int64_t>(p->n_cols, 1) * 4 + std::max<int64_t>(p->n_rows, 1) * 4)))
+        return cuda_status(e, "cudaMalloc");
+    float* dx = p->d_hx;
+    float* dy = p->d_hx + std::max<int64_t>(p->n_cols, 1);
     spmv_status s = SPMV_OK;
     if ((e = cudaMemcpyAsync(dx, xh, p->n_cols * 4, cudaMemcpyHostToDevice, st))) s = cuda_status(e, "H2D");
     if (!s) s = spmv_execute(p, dx, dy, stream);
     if (!s && (e = cudaMemcpyAsync(yh, dy, p->n_rows * 4, cudaMemcpyDeviceToHost, st))) s = cuda_status(e, "D2H");
-    cudaFreeAsync(dx, st); cudaFreeAsync(dy, st);
     if (!s && (e = cudaStreamSynchronize(st))) s = cuda_status(e, "sync");
     return s;
 }

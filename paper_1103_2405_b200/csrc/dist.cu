@@ -133,6 +133,8 @@ namespace {
 
 struct Dist {
     int P = 1, rank = 0;
+    uint8_t* d_half_local = nullptr;         // HITS: half flag per local row
+    uint8_t* d_col_half = nullptr;           // HITS: half flag per permuted column (k < nzc)
     int64_t n_local = 0, S = 0, slot = 0;    // owned rows, slot rows, slot floats (S + partials)
     int64_t nzc = 0;                         // local columns with entries (plan column prefix)
     std::vector<int64_t> gpos;               // vertex -> position in the gathered buffer
@@ -142,7 +144,7 @@ struct Dist {
     int32_t* d_idx = nullptr;                // x'[k] = G[idx[k]] for k < nzc
 };
 
-constexpr int64_t kPartialFloats = 8;        // two fp64 partials (+ padding), 16-byte multiple
+constexpr int64_t kPartialFloats = 8;        // four fp64 partials, 16-byte multiple
 
 __global__ void dist_permute(const float* __restrict__ G, const int32_t* __restrict__ idx,
                              float* __restrict__ xp, int64_t nzc, const tc::Ctrl* ctrl) {
@@ -183,6 +185,69 @@ __global__ void gather_rows(const float* p_e, const int32_t* fpos, float* slot, 
         slot[i] = fpos[i] >= 0 ? p_e[fpos[i]] : 0.0f;
 }
 
+// HITS (Eq. 8) row-partitioned: the slots carry the raw product y and the half sums; every rank
+// derives the same half norms (rank-order sums), normalises its own rows (post) and the gathered
+// x it reads (permute).  The L1 change of a normalisation travels with the next exchange, so the
+// stop decision lags one SpMV and the reported iterate is the one that converged (reading R14).
+__global__ void hits_dist_finalize(const float* G, int64_t slot, int64_t S, int P, tc::Ctrl* ctrl, int l2) {
+    if (threadIdx.x != 0 || *(volatile int32_t*)&ctrl->done) return;
+    double s0 = 0.0, s1 = 0.0, r = 0.0;
+    for (int k = 0; k < P; ++k) {
+        const double* part = reinterpret_cast<const double*>(G + (int64_t)k * slot + S);
+        s0 += part[0]; s1 += part[1]; r += part[2];
+    }
+    if (ctrl->iter >= 1) {
+        ctrl->residual = r;
+        const bool done = ctrl->fixed_iters > 0 ? ctrl->iter >= ctrl->fixed_iters
+                                                : (r < ctrl->tol || ctrl->iter >= ctrl->max_iter);
+        if (done) { ctrl->done = 1; return; }
+    }
+    ctrl->norm[0] = l2 ? sqrt(s0) : s0;
+    ctrl->norm[1] = l2 ? sqrt(s1) : s1;
+    ctrl->iter += 1;
+}
+
+// own rows: v = y / |y_half| (zero half -> uniform, R5); L1 change into the own slot's partial 2
+__global__ void __launch_bounds__(512) hits_dist_post(float* slot_y, float* v_old, const uint8_t* half, int64_t n_local,
+                                                      tc::Ctrl* ctrl, double* slots, double* res_out) {
+    if (*(volatile int32_t*)&ctrl->done) return;
+    const double n0 = ctrl->norm[0], n1 = ctrl->norm[1];
+    const float uni = (float)ctrl->uniform;
+    const float s0 = n0 > 0.0 ? (float)(1.0 / n0) : 0.0f, s1 = n1 > 0.0 ? (float)(1.0 / n1) : 0.0f;
+    double res = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += (int64_t)gridDim.x * blockDim.x) {
+        const int h = half[i];
+        const double nn = h ? n1 : n0;
+        const float vn = nn > 0.0 ? slot_y[i] * (h ? s1 : s0) : uni;
+        res += fabs((double)vn - (double)v_old[i]);
+        v_old[i] = vn;
+    }
+    double acc[1] = {res};
+    tc::block_reduce_to_slot<1>(acc, slots + blockIdx.x);
+    if (!tc::last_block(&ctrl->ticket)) return;
+    double s[1];
+    tc::block_sum_slots<1>(slots, gridDim.x, s);
+    if (threadIdx.x == 0) { ctrl->ticket = 0; *res_out = s[0]; }
+}
+
+__global__ void hits_dist_permute(const float* __restrict__ G, const int32_t* __restrict__ idx,
+                                  const uint8_t* __restrict__ col_half, float* __restrict__ xp, int64_t nzc,
+                                  const tc::Ctrl* ctrl) {
+    if (*(volatile const int32_t*)&ctrl->done) return;
+    const double n0 = ctrl->norm[0], n1 = ctrl->norm[1];
+    const float uni = (float)ctrl->uniform;
+    const float s0 = n0 > 0.0 ? (float)(1.0 / n0) : 0.0f, s1 = n1 > 0.0 ? (float)(1.0 / n1) : 0.0f;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nzc; k += (int64_t)gridDim.x * blockDim.x) {
+        const int h = col_half[k];
+        const double nn = h ? n1 : n0;
+        xp[k] = nn > 0.0 ? __ldg(G + __ldg(idx + k)) * (h ? s1 : s0) : uni;
+    }
+}
+
+__global__ void fill_f(float* a, int64_t n, float v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
+}
+
 spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
     if (c->world == 1) return SPMV_OK;
     return nccl_status(g_nccl.AllGather(G + (int64_t)c->rank * slot, G, (size_t)slot, ncclFloat32, c->comm, st),
@@ -197,7 +262,6 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
                                const spmv_options* opt_in, spmv_comm comm, int device,
                                spmv_solver* out) {
     (void)m;
-    if (algo == SPMV_ALGO_HITS) { set_error("row-partitioned HITS is not built in this version"); return SPMV_EINVAL; }
     cudaError_t e = cudaSetDevice(device);
     if (e) return cuda_status(e, "cudaSetDevice");
     spmv_solver_s* s = new spmv_solver_s();
@@ -210,7 +274,9 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         std::vector<int64_t> arp; std::vector<int32_t> acol;
         clean_adjacency(n, row_ptr, col, arp, acol);
         std::vector<int64_t> mrp, len; std::vector<int32_t> mcol;
-        build_iteration_matrix(algo, n, arp, acol, mrp, mcol, len);
+        const int64_t nv = n;
+        n = build_iteration_matrix(algo, nv, arp, acol, mrp, mcol, len);   // n := vector length N
+        s->N = n;
         // partition rows of M (bitonic over row lengths, Sec. 3.2)
         std::vector<int64_t> rl(n);
         for (int64_t i = 0; i < n; ++i) rl[i] = mrp[i + 1] - mrp[i];
@@ -265,7 +331,17 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         CKD(cudaMemcpy(s->d_inv, inv.data(), nl * sizeof(float), cudaMemcpyHostToDevice));
         CKD(cudaMalloc(&s->d_ctrl, sizeof(Ctrl)));
         CKD(cudaMemset(s->d_ctrl, 0, sizeof(Ctrl)));
-        CKD(setup_grids<EpiAffine>(*p, s->grids));
+        if (algo == SPMV_ALGO_HITS) {
+            std::vector<uint8_t> hl(nl, 0), ch(std::max<int64_t>(D->nzc, 1), 0);
+            for (int64_t r = 0; r < D->n_local; ++r) hl[r] = D->owned[r] >= nv;
+            for (int64_t k = 0; k < D->nzc; ++k) ch[k] = p->perm[k] >= nv;
+            CKD(cudaMalloc(&D->d_half_local, nl));
+            CKD(cudaMemcpy(D->d_half_local, hl.data(), nl, cudaMemcpyHostToDevice));
+            CKD(cudaMalloc(&D->d_col_half, ch.size()));
+            CKD(cudaMemcpy(D->d_col_half, ch.data(), ch.size(), cudaMemcpyHostToDevice));
+        }
+        if (algo == SPMV_ALGO_HITS) CKD(setup_grids<EpiHitsSpmv>(*p, s->grids));
+        else CKD(setup_grids<EpiAffine>(*p, s->grids));
         int32_t slots = 0;
         for (int32_t t = 0; t <= p->num_tiles; ++t) {
             if (p->tiles[t].wl_end == p->tiles[t].wl_begin) continue;
@@ -274,15 +350,21 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
             slots += s->grids[t];
         }
         s->total_slots = slots;
-        CKD(cudaMalloc(&s->d_slots, (size_t)std::max(slots, 1) * 2 * sizeof(double)));
+        CKD(cudaMalloc(&s->d_slots, (size_t)std::max(slots, p->sm_count * 4) * 2 * sizeof(double)));
         std::vector<uint32_t> entries;
         if ((st = plan_final_positions(p, entries, s->fpos))) throw st;
         const int64_t ne = std::max<int64_t>(p->n_row_entries, 1);
         std::vector<float> inv_e(ne, 0.0f);
+        std::vector<uint8_t> half_e(ne, 0);
         for (int64_t k = 0; k < p->n_row_entries; ++k) {
             const uint32_t ent = entries[k];
-            if (ent != PAD_ROW && (ent & FLAG_FINAL)) inv_e[k] = inv[ent & ROW_MASK];
+            if (ent != PAD_ROW && (ent & FLAG_FINAL)) {
+                inv_e[k] = inv[ent & ROW_MASK];
+                half_e[k] = D->owned[ent & ROW_MASK] >= nv;
+            }
         }
+        CKD(cudaMalloc(&s->d_half_e, ne));
+        CKD(cudaMemcpy(s->d_half_e, half_e.data(), ne, cudaMemcpyHostToDevice));
         CKD(cudaMalloc(&s->d_p_e, ne * sizeof(float)));
         CKD(cudaMalloc(&s->d_inv_e, ne * sizeof(float)));
         CKD(cudaMemcpy(s->d_inv_e, inv_e.data(), ne * sizeof(float), cudaMemcpyHostToDevice));
@@ -312,6 +394,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
         st = s->own_stream;
     }
     const int rwr = s->algo == SPMV_ALGO_RWR;
+    const int hitsa = s->algo == SPMV_ALGO_HITS;
     D->q_local = -1;
     if (rwr && (int32_t)(D->gpos[query] / D->slot) == D->rank) D->q_local = D->gpos[query] % D->slot;
     Ctrl c{};
@@ -319,14 +402,21 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     c.c = s->it.c; c.tol = s->it.tol; c.max_iter = s->it.max_iter; c.fixed_iters = s->it.fixed_iters;
     c.inv_n = 1.0 / n; c.residual = INFINITY; c.q = (int32_t)D->q_local;
     c.tele = rwr ? 0.0 : c.c * ((double)s->n_dangling / n) / n + (1.0 - c.c) / n;
+    c.uniform = s->it.hits_norm == 1 ? 1.0 / n : 1.0 / std::sqrt(n);
     if ((e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st))) return cuda_status(e, "ctrl");
     float* zslot = D->d_G + (int64_t)D->rank * D->slot;
     const int g = p->sm_count * 4;
-    dist_init<<<g, 256, 0, st>>>(s->d_p, zslot, s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
-    init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
-    spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
-    if (ss) return ss;
-    dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+    spmv_status ss = SPMV_OK;
+    if (hitsa) {   // a(0) = h(0) = 1/|V| (L440): own rows and every gathered column
+        fill_f<<<g, 256, 0, st>>>(s->d_p, D->n_local, (float)(1.0 / n));
+        fill_f<<<g, 256, 0, st>>>(p->d_xp, D->nzc, (float)(1.0 / n));
+        cudaMemsetAsync(zslot + D->S, 0, kPartialFloats * sizeof(float), st);
+    } else {
+        dist_init<<<g, 256, 0, st>>>(s->d_p, zslot, s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
+        init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
+        if ((ss = allgather(s->comm, D->d_G, D->slot, st))) return ss;
+        dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
@@ -337,6 +427,25 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     while (true) {
         for (int b = 0; b < batch; ++b) {
             const size_t nu = s->tiles_used.size();
+            if (hitsa) {
+                for (size_t i = 0; i < nu; ++i) {
+                    EpiHitsSpmv epi{};
+                    epi.y = zslot; epi.half = s->d_half_e; epi.fpos = s->d_fpos; epi.ctrl = s->d_ctrl;
+                    epi.slots = s->d_slots; epi.slot_base = s->slot_base[i]; epi.total_slots = s->total_slots;
+                    epi.is_last = (i + 1 == nu); epi.l2 = s->it.hits_norm != 1;
+                    epi.dist_out = reinterpret_cast<double*>(zslot + D->S);
+                    if ((e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], p->d_xp, epi, st)))
+                        return cuda_status(e, "tile launch");
+                }
+                if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
+                if ((ss = allgather(s->comm, D->d_G, D->slot, st))) return ss;
+                hits_dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->slot, D->S, D->P, s->d_ctrl, s->it.hits_norm != 1);
+                hits_dist_post<<<g, 512, 0, st>>>(zslot, s->d_p, D->d_half_local, D->n_local, s->d_ctrl, s->d_slots,
+                                                  reinterpret_cast<double*>(zslot + D->S) + 2);
+                hits_dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, D->d_col_half, p->d_xp, D->nzc, s->d_ctrl);
+                ++launched;
+                continue;
+            }
             for (size_t i = 0; i < nu; ++i) {
                 EpiAffine epi{};
                 epi.y = s->d_y; epi.p = s->d_p_e; epi.z_next = zslot; epi.inv_deg = s->d_inv_e;
@@ -376,12 +485,15 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     return SPMV_OK;
 }
 
-spmv_status solver_result_dist(spmv_solver s, float* out0, float*) {
+spmv_status solver_result_dist(spmv_solver s, float* out0, float* out1) {
     Dist* D = static_cast<Dist*>(s->dist);
     cudaSetDevice(s->device);
     cudaStream_t st = s->own_stream;
     float* slot = D->d_G + (int64_t)D->rank * D->slot;
-    gather_rows<<<s->plan->sm_count * 4, 256, 0, st>>>(s->d_p_e, s->d_fpos, slot, D->n_local);
+    if (s->algo == SPMV_ALGO_HITS)
+        cudaMemcpyAsync(slot, s->d_p, D->n_local * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    else
+        gather_rows<<<s->plan->sm_count * 4, 256, 0, st>>>(s->d_p_e, s->d_fpos, slot, D->n_local);
     spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
     if (ss) return ss;
     std::vector<float> G((size_t)D->P * D->slot);
@@ -389,13 +501,15 @@ spmv_status solver_result_dist(spmv_solver s, float* out0, float*) {
     if (!e) e = cudaStreamSynchronize(st);
     if (e) return cuda_status(e, "result");
     for (int64_t u = 0; u < s->n; ++u) out0[u] = G[D->gpos[u]];
+    if (s->algo == SPMV_ALGO_HITS)
+        for (int64_t u = 0; u < s->n; ++u) out1[u] = G[D->gpos[s->n + u]];
     return SPMV_OK;
 }
 
 void solver_destroy_dist(spmv_solver s) {
     Dist* D = static_cast<Dist*>(s->dist);
     cudaSetDevice(s->device);
-    if (D) { cudaFree(D->d_G); cudaFree(D->d_idx); delete D; }
+    if (D) { cudaFree(D->d_G); cudaFree(D->d_idx); cudaFree(D->d_half_local); cudaFree(D->d_col_half); delete D; }
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
     cudaFree(s->d_p); cudaFree(s->d_y); cudaFree(s->d_inv); cudaFree(s->d_ctrl); cudaFree(s->d_slots);
     cudaFree(s->d_p_e); cudaFree(s->d_inv_e); cudaFree(s->d_fpos);

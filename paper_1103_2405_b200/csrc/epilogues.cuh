@@ -145,6 +145,7 @@ struct EpiAffine {
 struct EpiHitsSpmv {
     float* y; const uint8_t* half;     // half: in row-entry order (fpos for split rows)
     const int32_t* fpos;
+    double* dist_out;                  // row-partitioned mode: last block writes the raw half sums
     Ctrl* ctrl; double* slots; int32_t slot_base, total_slots, is_last, l2;
     double s0, s1;
     __device__ __forceinline__ bool begin() {
@@ -179,6 +180,7 @@ struct EpiHitsSpmv {
         block_sum_slots<2>(slots, total_slots, s);
         if (threadIdx.x == 0) {
             ctrl->ticket = 0;
+            if (dist_out) { dist_out[0] = s[0]; dist_out[1] = s[1]; return; }
             ctrl->norm[0] = l2 ? sqrt(s[0]) : s[0];
             ctrl->norm[1] = l2 ? sqrt(s[1]) : s[1];
         }

@@ -37,6 +37,7 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
     a.col = p.d_col; a.val = p.d_val; a.row_id = p.d_row_id;
     a.x = xp + ti.col_lo; a.width = (int32_t)(ti.col_hi - ti.col_lo);
     a.hot = p.l1_hot_cols;
+    a.prefix = ti.staged ? 0 : (int32_t)std::min<int64_t>(p.x_prefix, ti.col_hi - ti.col_lo);
     a.split = p.d_split; a.partials = p.d_partials; a.counters = p.d_counters;
     if (p.stream) {
         WsArgs s;
@@ -62,8 +63,9 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
         if (p.pattern) tc_spmv_tile<true, false, Epi><<<grid, kThreads, smem, st>>>(a, epi);
         else tc_spmv_tile<true, true, Epi><<<grid, kThreads, smem, st>>>(a, epi);
     } else {
-        if (p.pattern) tc_spmv_tile<false, false, Epi><<<grid, kThreads, 0, st>>>(a, epi);
-        else tc_spmv_tile<false, true, Epi><<<grid, kThreads, 0, st>>>(a, epi);
+        const size_t smem = (size_t)a.prefix * sizeof(float);
+        if (p.pattern) tc_spmv_tile<false, false, Epi><<<grid, kThreads, smem, st>>>(a, epi);
+        else tc_spmv_tile<false, true, Epi><<<grid, kThreads, smem, st>>>(a, epi);
     }
     return cudaGetLastError();
 }
@@ -94,7 +96,9 @@ cudaError_t setup_grids(spmv_plan_s& p, std::vector<int>& grids) {
     const int max_dyn = optin - (int)fa.sharedSizeBytes;
     if ((e = cudaFuncSetAttribute(kst, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
     int nb = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kgl, kThreads, 0))) return e;
+    if ((e = cudaFuncSetAttribute(kgl, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
+    if (p.x_prefix * 4 > max_dyn) p.x_prefix = max_dyn / 4;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kgl, kThreads, (size_t)p.x_prefix * 4))) return e;
     const int g_global = std::max(1, nb) * p.sm_count;
     grids.assign(p.num_tiles + 1, g_global);
     for (int32_t t = 0; t <= p.num_tiles; ++t) {

@@ -28,6 +28,7 @@ struct spmv_plan_s {
     float* d_val = nullptr;
     int32_t* d_perm = nullptr;
     float* d_xp = nullptr;          // relabelled x for spmv_execute
+    float* d_hx = nullptr;          // spmv_execute_host staging (x then y)
     int32_t* d_split = nullptr;
     float* d_partials = nullptr;
     int32_t* d_counters = nullptr;
@@ -37,6 +38,7 @@ struct spmv_plan_s {
     bool stream = true;
     int32_t stage_slots = 0;                  // slots per warp buffer (largest workload)
     int stream_grid = 0;
+    int32_t x_prefix = 0;                  // unstaged tiles: x columns staged in shared memory
     int32_t l1_hot_cols = 0;               // see TileArgs::hot; 0 = plain ld.global.nc (TCSPMV_L1_HOT)
     int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore

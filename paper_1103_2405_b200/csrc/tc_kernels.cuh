@@ -67,6 +67,8 @@ struct TileArgs {
     int32_t width;            // tile width = padding sentinel
     int32_t hot;              // unstaged tiles: columns below are gathered with L1 evict-last,
                               // the rest evict-first (the relabelled hub columns stay in L1)
+    int32_t prefix;           // unstaged tiles: the first `prefix` columns (the tile's densest,
+                              // Solution 2 order) are staged in shared memory, the rest gathered
     const int32_t* split;     // [n_split][3]
     float* partials;          // [n_chunks]
     int32_t* counters;        // [n_split], zero between launches
@@ -110,9 +112,11 @@ struct XSrc {
     const float* s;     // shared base
     int32_t width;
     int32_t hot;
+    int32_t prefix;
     __device__ __forceinline__ float operator()(int32_t c) const {
         if (c == width) return 0.0f;                  // padding slot (sentinel, reading R16)
         if (STAGED) return s[c];
+        if (c < prefix) return s[c];
         if (hot <= 0) return __ldg(g + c);
         float v;
         if (c < hot) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
@@ -351,10 +355,10 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
     extern __shared__ float xs[];
     Epi epi = epi_in;
     if (!epi.begin()) return;                         // iteration loop already converged
-    if (STAGED) {
-        // stage the tile's x segment once per CTA (float4 where aligned)
+    if (STAGED || a.prefix > 0) {
+        // stage the tile's x segment (or its dense prefix) once per CTA (float4 where aligned)
         const float* src = a.x;
-        const int n = a.width;
+        const int n = STAGED ? a.width : a.prefix;
         const int head = (int)((4 - ((reinterpret_cast<uintptr_t>(src) >> 2) & 3)) & 3);
         const int h = head < n ? head : n;
         for (int i = threadIdx.x; i < h; i += kThreads) xs[i] = __ldg(src + i);
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         for (int i = h + 4 * n4 + threadIdx.x; i < n; i += kThreads) xs[i] = __ldg(src + i);
         __syncthreads();
     }
-    XSrc<STAGED> x{a.x, xs, a.width, a.hot};
+    XSrc<STAGED> x{a.x, xs, a.width, a.hot, STAGED ? 0 : a.prefix};
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * kWarps;
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) tc_spmv_wstream(TileArgs a,
     WlDesc d = j < a.wl_end ? load_desc(a.desc + j) : WlDesc{};
     if (lane == 0 && j < a.wl_end) ws_issue<VALUED>(a, d, cbuf[0], vbuf[0], bars + 2 * warp, pol);
     if (STAGED) mbar_wait(xbar, 0);
-    XSrc<STAGED> x{a.x, xs, a.width, a.hot};
+    XSrc<STAGED> x{a.x, xs, a.width, a.hot, 0};
     for (int k = 0; j < a.wl_end; j += G, ++k) {
         const int cur = k & 1;
         const int64_t jn = j + G;

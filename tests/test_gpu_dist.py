@@ -43,8 +43,17 @@ def test_dist_rwr_world1(gpu):
     assert np.abs(r - ref).sum() < 1e-6, info
 
 
-def test_dist_hits_not_built(gpu):
-    from paper_1103_2405_b200 import Solver, SpmvError
+@pytest.mark.parametrize("norm", [1, 2])
+def test_dist_hits_world1(norm, gpu):
+    from paper_1103_2405_b200 import Solver
     G = graphgen.make_graph("t_small")
-    with pytest.raises(SpmvError, match="EINVAL"):
-        Solver("hits", G.n, G.row_ptr, G.col, device=0, comm=comm1())
+    s = Solver("hits", G.n, G.row_ptr, G.col, device=0, comm=comm1(), iter_kw=dict(hits_norm=norm))
+    info = s.run()
+    a, h = s.result()
+    ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=norm, fixed_iters=info["iterations"])
+    bar_a = 1e-6 * (1.0 if norm == 1 else np.abs(ra).sum())
+    bar_h = 1e-6 * (1.0 if norm == 1 else np.abs(rh).sum())
+    assert np.abs(a - ra).sum() < bar_a and np.abs(h - rh).sum() < bar_h, info
+    # the same number of normalisations as the single-GPU solver
+    s1 = Solver("hits", G.n, G.row_ptr, G.col, device=0, iter_kw=dict(hits_norm=norm))
+    assert abs(s1.run()["iterations"] - info["iterations"]) <= 1
