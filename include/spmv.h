@@ -185,6 +185,16 @@ spmv_status spmv_solver_plan_stats(spmv_solver s, spmv_plan_stats_t* out);
 int32_t spmv_solver_launches_per_iter(spmv_solver s);
 void spmv_solver_destroy(spmv_solver s);
 
+/* Batched RWR (the paper's 25 random queries, L448): the Q <= 32 queries of an
+ * RWR solver iterate together as one SpMM over the same layout (lanes = queries: one 128-byte x
+ * row per stored entry instead of Q random gathers).  The loop runs until every query's L1 change
+ * is below tol (or fixed_iters); res->residual is the largest.  Synchronises.
+ * Errors: EINVAL (not an RWR solver, multi-GPU solver, Q outside [1, 32]), ERANGE (query). */
+spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t Q, void* stream,
+                                  spmv_iter_result* res);
+/* The batched results, query-major: out[q * n + u] = r_q(u), caller order. */
+spmv_status spmv_solver_result_batch(spmv_solver s, float* out);
+
 /* One-shot wrappers: create, run, copy result, destroy. */
 spmv_status pagerank(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* col,
                      const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,

@@ -201,6 +201,22 @@ class Solver:
                     ms_total=r.ms_total, us_per_iter=r.us_per_iter,
                     predicted_us_per_iter=r.predicted_us_per_iter)
 
+    def run_batch(self, queries, stream=None) -> dict:
+        """Batched RWR: all queries (<= 32) iterate together (spmv_solver_run_batch)."""
+        q = _np(queries, np.int64)
+        self._nq = len(q)
+        r = C.IterResult()
+        st = C.lib().spmv_solver_run_batch(self._h, q.ctypes.data, len(q), _stream_handle(stream), ctypes.byref(r))
+        if st not in (0, 10):
+            check(st, "spmv_solver_run_batch")
+        return dict(iterations=r.iterations, converged=bool(r.converged), residual=r.residual,
+                    ms_total=r.ms_total, us_per_iter=r.us_per_iter)
+
+    def result_batch(self) -> np.ndarray:
+        out = np.zeros((self._nq, self.n), np.float32)
+        check(C.lib().spmv_solver_result_batch(self._h, out.ctypes.data), "spmv_solver_result_batch")
+        return out
+
     def result(self):
         a = np.zeros(max(self.n, 1), np.float32)
         b = np.zeros(max(self.n, 1), np.float32)

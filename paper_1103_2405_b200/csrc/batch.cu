@@ -1,0 +1,359 @@
+// batch.cu -- batched Random Walk with Restart (the
+// paper averages 25 random query nodes).  The Q <= 32 queries iterate together as one SpMM
+// Y = W R over the same tiled-composite layout: lanes are queries, so every stored entry costs one
+// coalesced 128-byte read of an x row (all queries' values of that column) instead of a random
+// 4-byte gather per query.  Rows are written as 128-byte rows too.  Everything else (tiles in
+// fixed order, first-touch/accumulate flags, split chunks combined in chunk order, fp64 per-query
+// partial sums reduced in a fixed order, device-side WHILE loop) follows the single-query path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "epilogues.cuh"
+#include "launch.cuh"
+#include "solver.h"
+
+namespace tc {
+
+constexpr int kQP = 32;                 // padded queries per row (one per lane)
+
+struct BatchArgs {
+    const WlDesc* desc;
+    int64_t wl_begin, wl_end;
+    const int32_t* col;
+    const uint32_t* row_id;
+    int64_t col_lo;                     // tile's first relabelled column
+    int32_t width;                      // sentinel
+    const int32_t* split;               // [n_split][3]
+    float* partials;                    // [n_chunks][32]
+    int32_t* counters;                  // [n_split]
+    const float* Z;                     // [N][32] input (r * inv_deg)
+    float* Znext;                       // [N][32]
+    float* R;                           // [N][32] current iterate (updated in place)
+    float* Y;                           // [N][32] partial sums of rows shared by several tiles
+    const float* inv;                   // [N]
+    const int32_t* q;                   // [32] relabelled query per lane (-1: padding lane)
+    float c;
+    Ctrl* ctrl;
+    double* slots;                      // [grid][32] per-block residual partials
+    double* res_out;                    // [32]
+    int32_t slot_base, total_slots, is_last;
+    cudaGraphConditionalHandle cond;
+};
+
+struct BatchEpi {
+    const BatchArgs& a;
+    int lane;
+    double& res;
+    __device__ __forceinline__ void write(uint32_t ent, float v) {
+        if (ent == PAD_ROW) return;
+        const uint32_t r = ent & ROW_MASK;
+        const int64_t o = (int64_t)r * kQP + lane;
+        if (ent & FLAG_ACC) v += a.Y[o];
+        if (!(ent & FLAG_FINAL)) { a.Y[o] = v; return; }
+        float rn = a.c * v;
+        if ((int32_t)r == a.q[lane]) rn += 1.0f - a.c;       // Eq. 9: + (1-c) e_q
+        res += fabs((double)rn - (double)a.R[o]);
+        a.R[o] = rn;
+        a.Znext[o] = rn * __ldg(a.inv + r);
+    }
+};
+
+__device__ __forceinline__ float xrow(const BatchArgs& a, int32_t c, int lane) {
+    if (c == a.width) return 0.0f;
+    return __ldg(a.Z + (a.col_lo + c) * kQP + lane);
+}
+
+// one row of `len` slots starting at cb (row major / split chunk); all lanes see every slot
+__device__ __forceinline__ float row_dot(const BatchArgs& a, const int32_t* cb, int len, int lane) {
+    float acc = 0.0f;
+    for (int k0 = 0; k0 < len; k0 += 32) {
+        const int32_t cl = (k0 + lane < len) ? __ldcs(cb + k0 + lane) : a.width;
+        // all 32 x rows of the chunk in flight before the sum (padding -> sentinel -> 0)
+        float xv[32];
+        #pragma unroll
+        for (int j = 0; j < 32; ++j) xv[j] = xrow(a, __shfl_sync(0xffffffffu, cl, j), lane);
+        #pragma unroll
+        for (int j = 0; j < 32; ++j) acc += xv[j];
+    }
+    return acc;
+}
+
+template <int KV>
+__device__ __forceinline__ void slab_round(const BatchArgs& a, const int32_t* sb, int p0, float (&acc)[32], int lane) {
+    // positions p0 .. p0+31 of a k-interleaved slab: row rr = (p % (32 KV)) / KV
+    const int32_t cl = __ldcs(sb + p0 + lane);
+    const int base = (p0 % (32 * KV)) / KV;
+    float xv[32];
+    #pragma unroll
+    for (int j = 0; j < 32; ++j) xv[j] = xrow(a, __shfl_sync(0xffffffffu, cl, j), lane);
+    // rr = base + j / KV, with base in {0, 32/KV, ...}: dispatch on base keeps acc indices static
+    #pragma unroll
+    for (int b = 0; b < KV; ++b) {
+        if (base != b * (32 / KV)) continue;
+        #pragma unroll
+        for (int j = 0; j < 32; ++j) acc[b * (32 / KV) + j / KV] += xv[j];
+    }
+}
+
+__global__ void __launch_bounds__(512, 1) spmm_rwr_tile(BatchArgs a) {
+    if (*(volatile int32_t*)&a.ctrl->done) return;
+    const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+    const int64_t G = (int64_t)gridDim.x * warps;
+    double res = 0.0;
+    BatchEpi epi{a, lane, res};
+    for (int64_t j = a.wl_begin + gw; j < a.wl_end; j += G) {
+        const WlDesc d = load_desc(a.desc + j);
+        const int32_t* wc = a.col + d.off;
+        if (d.kind != KIND_CM) {
+            for (int r = 0; r < d.h; ++r) {
+                const float v = row_dot(a, wc + (int64_t)r * d.w, d.w, lane);
+                const uint32_t ent = __ldg(a.row_id + d.row_base + r);
+                if (d.kind == KIND_SPLIT) {
+                    const int32_t* sp = a.split + 3 * d.split_id;
+                    const int32_t nch = __ldg(sp + 1), pbase = __ldg(sp + 2);
+                    a.partials[(int64_t)(pbase + d.chunk) * kQP + lane] = v;
+                    __threadfence();
+                    __syncwarp();
+                    int32_t t = 0;
+                    if (lane == 0) t = atomicAdd(a.counters + d.split_id, 1);
+                    t = __shfl_sync(0xffffffffu, t, 0);
+                    if (t == nch - 1) {
+                        __threadfence();
+                        float s = 0.0f;
+                        for (int32_t c = 0; c < nch; ++c) s += __ldcg(a.partials + (int64_t)(pbase + c) * kQP + lane);
+                        __syncwarp();
+                        if (lane == 0) a.counters[d.split_id] = 0;
+                        epi.write(ent, s);
+                    }
+                } else {
+                    epi.write(ent, v);
+                }
+            }
+        } else {
+            const int slabs = d.h >> 5;
+            for (int s = 0; s < slabs; ++s) {
+                float acc[32];
+                #pragma unroll
+                for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+                const int32_t* sb = wc + (int64_t)s * 32 * d.w;
+                const int npos = 32 * d.w;
+                for (int p0 = 0; p0 < npos; p0 += 32) {
+                    if (d.kvec == 4) slab_round<4>(a, sb, p0, acc, lane);
+                    else if (d.kvec == 2) slab_round<2>(a, sb, p0, acc, lane);
+                    else slab_round<1>(a, sb, p0, acc, lane);
+                }
+                const uint32_t myent = __ldg(a.row_id + d.row_base + s * 32 + lane);
+                #pragma unroll
+                for (int rr = 0; rr < 32; ++rr) epi.write(__shfl_sync(0xffffffffu, myent, rr), acc[rr]);
+            }
+        }
+    }
+    // per-query residual: fixed-order block reduction over warps, then over blocks
+    __shared__ double red[16][32];
+    const int w = threadIdx.x >> 5;
+    red[w][lane] = res;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double s = 0.0;
+        for (int k = 0; k < warps; ++k) s += red[k][threadIdx.x];
+        a.slots[(int64_t)(a.slot_base + blockIdx.x) * 32 + threadIdx.x] = s;
+    }
+    if (!a.is_last) return;
+    if (!last_block(&a.ctrl->ticket)) return;
+    if (threadIdx.x < 32) {
+        double s = 0.0;
+        for (int b = 0; b < a.total_slots; ++b) s += __ldcg(a.slots + (int64_t)b * 32 + threadIdx.x);
+        a.res_out[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.ctrl->ticket = 0;
+        double worst = 0.0;
+        for (int l = 0; l < 32; ++l)
+            if (a.q[l] >= 0) worst = fmax(worst, a.res_out[l]);
+        const bool done = iteration_done(a.ctrl, worst);
+        __threadfence();
+        set_cond(a.cond, !done);
+    }
+}
+
+__global__ void spmm_init(float* R, float* Z, const float* inv, const int32_t* q, int64_t N) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N * kQP; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / kQP;
+        const int l = (int)(i % kQP);
+        const float v = (q[l] >= 0 && r == q[l]) ? 1.0f : 0.0f;   // r(0) = e_q (reading R7)
+        R[i] = v;
+        Z[i] = v * inv[r];
+    }
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+struct BatchState {
+    float *R = nullptr, *Z[2] = {nullptr, nullptr}, *Y = nullptr, *partials = nullptr;
+    int32_t* q = nullptr;
+    double *slots = nullptr, *res = nullptr;
+    int32_t Q = 0;
+    int64_t N = 0;
+    std::vector<int> grids;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<double> residual;
+};
+
+static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int parity, int32_t slot_base,
+                            int32_t total_slots, bool is_last, cudaGraphConditionalHandle cond) {
+    spmv_plan_s* p = s->plan;
+    const TileInfo& ti = p->tiles[t];
+    BatchArgs a{};
+    a.desc = p->d_desc; a.wl_begin = ti.wl_begin; a.wl_end = ti.wl_end;
+    a.col = p->d_col; a.row_id = p->d_row_id; a.col_lo = ti.col_lo;
+    a.width = (int32_t)(ti.col_hi - ti.col_lo);
+    a.split = p->d_split; a.partials = B->partials; a.counters = p->d_counters;
+    a.Z = B->Z[parity]; a.Znext = B->Z[parity ^ 1]; a.R = B->R; a.Y = B->Y; a.inv = s->d_inv;
+    a.q = B->q; a.c = (float)s->it.c; a.ctrl = s->d_ctrl; a.slots = B->slots; a.res_out = B->res;
+    a.slot_base = slot_base; a.total_slots = total_slots; a.is_last = is_last; a.cond = cond;
+    return a;
+}
+
+static cudaError_t enqueue_batch_iteration(spmv_solver_s* s, BatchState* B, int parity, cudaStream_t st,
+                                           cudaGraphConditionalHandle cond) {
+    const size_t nu = s->tiles_used.size();
+    int32_t total = 0;
+    for (size_t i = 0; i < nu; ++i) total += s->plan->sm_count;
+    int32_t base = 0;
+    for (size_t i = 0; i < nu; ++i) {
+        BatchArgs a = batch_args(s, B, s->tiles_used[i], parity, base, total, i + 1 == nu, cond);
+        spmm_rwr_tile<<<s->plan->sm_count, 512, 0, st>>>(a);
+        base += s->plan->sm_count;
+        cudaError_t e = cudaGetLastError();
+        if (e) return e;
+    }
+    return cudaSuccess;
+}
+
+extern "C" {
+
+__attribute__((visibility("default")))
+spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t Q, void* stream,
+                                  spmv_iter_result* res) {
+    if (!s || !queries || Q < 1 || Q > kQP) { set_error("invalid argument (1 <= Q <= 32)"); return SPMV_EINVAL; }
+    if (s->algo != SPMV_ALGO_RWR || s->comm) { set_error("batched runs are single-GPU RWR"); return SPMV_EINVAL; }
+    for (int32_t i = 0; i < Q; ++i)
+        if (queries[i] < 0 || queries[i] >= s->n) { set_error("query out of range"); return SPMV_ERANGE; }
+    cudaError_t e = cudaSetDevice(s->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!st) {
+        if (!s->own_stream && (e = cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking)))
+            return cuda_status(e, "stream");
+        st = s->own_stream;
+    }
+    BatchState* B = static_cast<BatchState*>(s->batch);
+    spmv_plan_s* p = s->plan;
+    if (!B) {
+        B = new BatchState();
+        s->batch = B;
+        B->N = s->N;
+        const size_t vec = (size_t)(s->N + 4) * kQP * sizeof(float);
+#define CKB(x) do { if ((e = (x)) != cudaSuccess) return cuda_status(e, #x); } while (0)
+        CKB(cudaMalloc(&B->R, vec));
+        CKB(cudaMalloc(&B->Z[0], vec));
+        CKB(cudaMalloc(&B->Z[1], vec));
+        CKB(cudaMemset(B->Z[0], 0, vec));
+        CKB(cudaMemset(B->Z[1], 0, vec));
+        if (p->num_tiles > 0) CKB(cudaMalloc(&B->Y, vec));
+        CKB(cudaMalloc(&B->partials, (size_t)std::max<int64_t>(p->n_chunks, 1) * kQP * sizeof(float)));
+        CKB(cudaMalloc(&B->q, kQP * sizeof(int32_t)));
+        const size_t nslots = (size_t)std::max<size_t>(s->tiles_used.size(), 1) * p->sm_count;
+        CKB(cudaMalloc(&B->slots, nslots * kQP * sizeof(double)));
+        CKB(cudaMalloc(&B->res, kQP * sizeof(double)));
+        // device-side loop: WHILE node around two iterations (double-buffered input)
+        cudaGraph_t g;
+        CKB(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CKB(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CKB(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CKB(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        cudaError_t e1 = enqueue_batch_iteration(s, B, 0, st, h);
+        cudaError_t e2 = enqueue_batch_iteration(s, B, 1, st, h);
+        cudaGraph_t cap = nullptr;
+        e = cudaStreamEndCapture(st, &cap);
+        if (e1) return cuda_status(e1, "capture");
+        if (e2) return cuda_status(e2, "capture");
+        if (e) return cuda_status(e, "cudaStreamEndCapture");
+        CKB(cudaGraphInstantiate(&B->exec, g, 0));
+        B->graph = g;
+#undef CKB
+    }
+    B->Q = Q;
+    std::vector<int32_t> hq(kQP, -1);
+    for (int32_t i = 0; i < Q; ++i) hq[i] = s->pi[queries[i]];
+    Ctrl c{};
+    c.c = s->it.c; c.tol = s->it.tol; c.max_iter = s->it.max_iter; c.fixed_iters = s->it.fixed_iters;
+    c.inv_n = 1.0 / (double)s->n; c.residual = INFINITY; c.q = -1;
+    if ((e = cudaMemcpyAsync(B->q, hq.data(), kQP * sizeof(int32_t), cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st)))
+        return cuda_status(e, "upload");
+    spmm_init<<<p->sm_count * 8, 256, 0, st>>>(B->R, B->Z[0], s->d_inv, B->q, s->N);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    e = cudaGraphLaunch(B->exec, st);
+    cudaEventRecord(e1, st);
+    B->residual.assign(kQP, 0.0);
+    if (!e) e = cudaMemcpyAsync(&c, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaMemcpyAsync(B->residual.data(), B->res, kQP * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    if (e) return cuda_status(e, "batched loop");
+    if (res) {
+        res->iterations = c.iter; res->residual = c.residual;
+        res->converged = s->it.fixed_iters > 0 ? 1 : (c.residual < s->it.tol);
+        res->ms_total = ms; res->us_per_iter = c.iter ? 1000.0 * ms / c.iter : 0.0;
+        res->predicted_us_per_iter = p->predicted_us;
+    }
+    if (s->it.fixed_iters <= 0 && !(c.residual < s->it.tol)) { set_error("max_iter reached"); return SPMV_ENOCONV; }
+    return SPMV_OK;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_solver_result_batch(spmv_solver s, float* out) {
+    if (!s || !out || !s->batch) { set_error("no batched run"); return SPMV_EINVAL; }
+    BatchState* B = static_cast<BatchState*>(s->batch);
+    std::vector<float> R((size_t)s->N * kQP);
+    cudaSetDevice(s->device);
+    cudaError_t e = cudaMemcpy(R.data(), B->R, R.size() * sizeof(float), cudaMemcpyDeviceToHost);
+    if (e) return cuda_status(e, "result");
+    for (int32_t qi = 0; qi < B->Q; ++qi)
+        for (int64_t u = 0; u < s->n; ++u) out[(size_t)qi * s->n + u] = R[(size_t)s->pi[u] * kQP + qi];
+    return SPMV_OK;
+}
+
+}  // extern "C"
+
+void batch_destroy(spmv_solver s) {
+    BatchState* B = static_cast<BatchState*>(s->batch);
+    if (!B) return;
+    if (B->exec) cudaGraphExecDestroy(B->exec);
+    if (B->graph) cudaGraphDestroy(B->graph);
+    cudaFree(B->R); cudaFree(B->Z[0]); cudaFree(B->Z[1]); cudaFree(B->Y); cudaFree(B->partials);
+    cudaFree(B->q); cudaFree(B->slots); cudaFree(B->res);
+    delete B;
+    s->batch = nullptr;
+}

@@ -318,6 +318,7 @@ __attribute__((visibility("default"))) void spmv_solver_destroy(spmv_solver s) {
     if (!s) return;
     if (s->comm) { solver_destroy_dist(s); return; }
     cudaSetDevice(s->device);
+    batch_destroy(s);
     if (s->exec) cudaGraphExecDestroy(s->exec);
     if (s->graph) cudaGraphDestroy(s->graph);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);

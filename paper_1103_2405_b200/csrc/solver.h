@@ -60,6 +60,7 @@ struct spmv_solver_s {
     cudaStream_t own_stream = nullptr;
     tc::Ctrl last{};
     spmv_comm comm = nullptr;       // multi-GPU solvers (dist.cu)
+    void* batch = nullptr;          // batched RWR state (batch.cu)
     void* dist = nullptr;
 };
 
@@ -71,3 +72,4 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
 spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res);
 spmv_status solver_result_dist(spmv_solver s, float* out0, float* out1);
 void solver_destroy_dist(spmv_solver s);
+void batch_destroy(spmv_solver s);

@@ -90,3 +90,27 @@ def test_fixed_iters_and_c0(gpu):
     s = Solver("pagerank", G.n, G.row_ptr, G.col, device=0, iter_kw=dict(c=0.0, fixed_iters=1))
     s.run()
     assert np.allclose(s.result(), 1.0 / G.n, rtol=1e-6)
+
+
+@pytest.mark.parametrize("opt", range(len(OPTS)))
+def test_rwr_batch_parity(opt, gpu):
+    """Batched RWR (f1): every query of the batch equals the oracle run for the batch's
+    iteration count; the batch stops when the slowest query converges."""
+    from paper_1103_2405_b200 import Solver
+    for name, G in graphs()[:3]:
+        s = Solver("rwr", G.n, G.row_ptr, G.col, device=0, **OPTS[opt])
+        deg = np.diff(G.row_ptr) + np.bincount(G.col, minlength=G.n)
+        cand = np.nonzero(deg > 0)[0]
+        rng = np.random.default_rng(graphgen.SEED_QUERY)
+        qs = rng.choice(cand, size=min(7, len(cand)), replace=False)
+        info = s.run_batch(qs)
+        R = s.result_batch()
+        worst = 0.0
+        for i, q in enumerate(qs):
+            ref, rr = oracle.rwr(G.n, G.row_ptr, G.col, int(q), fixed_iters=info["iterations"])
+            err = np.abs(R[i].astype(np.float64) - ref).sum()
+            assert err < L1_BAR, (name, q, err, info)
+            worst = max(worst, rr.residual)
+        assert abs(worst - info["residual"]) < 1e-6
+        # a single-query run of the same solver still works after the batch
+        s.run(int(qs[0]))
