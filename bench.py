@@ -202,7 +202,9 @@ def main():
     tiles = [t for t in range(st["num_tiles"] + 1) if st["tile_nnz"][t] > 0 or t == st["num_tiles"]]
     launch_bytes = [12.0 * G.n]
     launch_names = ["permute_x"]
+    launch_nnz = [0]
     for t in tiles[: nl - 1]:
+        launch_nnz.append(st["tile_nnz"][t])
         width = st["tile_col_hi"][t] - st["tile_col_lo"][t]
         launch_bytes.append(8.0 * st["tile_nnz"][t] + 8.0 * st["tile_rows"][t] + 4.0 * width)
         launch_names.append(f"tc_spmv_tile[{t}]" + ("(smem x)" if st["tile_staged"][t] else "(L1/L2 x)"))
@@ -214,6 +216,23 @@ def main():
                 "kernel_share": round(float(per[dom] / per.sum()), 3), "peak_source": peak_src,
                 "per_launch_us": [round(float(v) * 1e3, 2) for v in per],
                 "launch_names": launch_names}
+    # the ceiling that binds on B200: random x gathers per second, measured by
+    # bench/probe/probe.cu on an x of the closest size (skewed columns, L1-allocating loads)
+    try:
+        best = None
+        with open(os.path.join(ROOT, "profiles", "r01_probe_gather.jsonl")) as f:
+            for ln in f:
+                r = json.loads(ln)
+                if r.get("probe") == "gather" and r.get("dist") == "skew" and r.get("mode") == 0:
+                    if best is None or abs(np.log(r["S"] / G.n)) < abs(np.log(best["S"] / G.n)):
+                        best = r
+        if best is not None and launch_nnz[dom] > 0:
+            g_ach = launch_nnz[dom] / (per[dom] * 1e-3) / 1e9
+            roofline["gather"] = {"achieved_G_per_s": round(g_ach, 1), "probe_G_per_s": best["Ggather_s"],
+                                  "frac": round(g_ach / best["Ggather_s"], 3),
+                                  "probe": "profiles/r01_probe_gather.jsonl skew S=%d" % best["S"]}
+    except Exception:
+        pass
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f).get(launch_names[dom].split("(")[0])
@@ -260,6 +279,15 @@ def main():
             extras[f"{algo}_iters_per_s"] = round(1e3 * info["iterations"] / info["ms_total"], 1)
             extras[f"{algo}_iterations"] = info["iterations"]
             extras[f"{algo}_us_per_iter"] = round(info["us_per_iter"], 2)
+            if algo == "rwr":
+                # the paper's 25 random queries (L448), batched as one SpMM per iteration (f1)
+                deg = np.diff(G.row_ptr) + np.bincount(G.col, minlength=G.n)
+                rng = np.random.default_rng(graphgen.SEED_QUERY)
+                qs = rng.choice(np.nonzero(deg > 0)[0], size=25, replace=False)
+                s.run_batch(qs)
+                bi = s.run_batch(qs)
+                extras["rwr_batch25_us_per_iter"] = round(bi["us_per_iter"], 1)
+                extras["rwr_batch25_query_iters_per_s"] = round(25 * 1e6 / bi["us_per_iter"], 1)
             s.close()
         # cpu_baseline: the oracle as it stands on this box's host cores, bounded sample
         import oracle

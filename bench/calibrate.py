@@ -120,7 +120,7 @@ def main():
     out = {"version": 1, "device": torch.cuda.get_device_name(0),
            "sms": torch.cuda.get_device_properties(0).multi_processor_count,
            "max_act_warp": int(warps), "launch_us": round(launch_us, 3),
-           "stage_GBps": 6000.0, "rmw_GBps": 4000.0,
+           "stage_GBps": 6000.0, "rmw_GBps": 4000.0, "tail_frac": 0.5,
            "units": "slots per second, whole GPU, every warp on one (w,h) shape (reading R20)",
            "columns": ["x mode (0 uncached uniform, 1 cached, 2 uncached power-law)", "valued", "kind(0=rm,1=cm)", "w", "h", "slots_per_s"],
            "entries": entries}

@@ -52,7 +52,7 @@ static void free_device(spmv_plan_s* p) {
     cudaSetDevice(p->device);
     cudaFree(p->d_desc); cudaFree(p->d_row_id); cudaFree(p->d_col); cudaFree(p->d_val);
     cudaFree(p->d_perm); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
-    cudaFree(p->d_counters); cudaFree(p->d_hx);
+    cudaFree(p->d_counters); cudaFree(p->d_hx); cudaFree(p->d_sched);
     cudaSetDevice(cur);
 }
 
@@ -125,12 +125,15 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
         std::vector<float> zf(std::max<int64_t>(p->n_chunks, 1), 0.0f);
         std::vector<int32_t> zi(std::max<int64_t>(p->n_split, 1), 0);
         std::vector<float> xpz(p->n_cols + 4, 0.0f);
+        std::vector<uint32_t> zs((size_t)(tc::kDynQ + 1) * (p->num_tiles + 1), 0u);
         if ((e = upload(&p->d_partials, zf, b)) || (e = upload(&p->d_counters, zi, b)) ||
+            (e = upload(&p->d_sched, zs, b)) ||
             (e = upload(&p->d_xp, xpz, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
         if (const char* h = std::getenv("TCSPMV_L1_HOT")) p->l1_hot_cols = std::atoi(h);
         if (const char* h = std::getenv("TCSPMV_PREFIX")) p->x_prefix = std::atoi(h) / 4 * 4;
+        if (const char* h = std::getenv("TCSPMV_CARVEOUT")) p->l1_carveout = std::atoi(h);
         const char* kenv = std::getenv("TCSPMV_KERNEL");
         p->stream = kenv && std::string(kenv) == "stream";
         if (p->stream && (e = build_stream_tables(p))) {

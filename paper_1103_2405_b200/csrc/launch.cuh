@@ -39,6 +39,7 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
     a.hot = p.l1_hot_cols;
     a.prefix = ti.staged ? 0 : (int32_t)std::min<int64_t>(p.x_prefix, ti.col_hi - ti.col_lo);
     a.split = p.d_split; a.partials = p.d_partials; a.counters = p.d_counters;
+    a.sched = p.d_sched + (kDynQ + 1) * t;
     if (p.stream) {
         WsArgs s;
         size_t smem = 0;
@@ -97,6 +98,9 @@ cudaError_t setup_grids(spmv_plan_s& p, std::vector<int>& grids) {
     if ((e = cudaFuncSetAttribute(kst, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
     int nb = 0;
     if ((e = cudaFuncSetAttribute(kgl, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
+    // unstaged tiles gather x through L1: ask for the largest L1 (smallest shared carve-out)
+    if (p.x_prefix == 0 && p.l1_carveout >= 0 &&
+        (e = cudaFuncSetAttribute(kgl, cudaFuncAttributePreferredSharedMemoryCarveout, p.l1_carveout))) return e;
     if (p.x_prefix * 4 > max_dyn) p.x_prefix = max_dyn / 4;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kgl, kThreads, (size_t)p.x_prefix * 4))) return e;
     const int g_global = std::max(1, nb) * p.sm_count;

@@ -32,12 +32,14 @@ struct spmv_plan_s {
     int32_t* d_split = nullptr;
     float* d_partials = nullptr;
     int32_t* d_counters = nullptr;
+    uint32_t* d_sched = nullptr;    // [(kDynQ + 1) * (num_tiles + 1)] dynamic-schedule counters
     int64_t device_bytes = 0;
     int sm_count = 0;
     // streaming kernel (per-warp bulk-copy double buffers)
     bool stream = true;
     int32_t stage_slots = 0;                  // slots per warp buffer (largest workload)
     int stream_grid = 0;
+    int32_t l1_carveout = -1;              // TCSPMV_CARVEOUT: preferred shared-memory carve-out (%)
     int32_t x_prefix = 0;                  // unstaged tiles: x columns staged in shared memory
     int32_t l1_hot_cols = 0;               // see TileArgs::hot; 0 = plain ld.global.nc (TCSPMV_L1_HOT)
     int max_dyn_smem = 0;

@@ -51,9 +51,13 @@ namespace tc {
 #ifndef TC_CM_SLOTS_P_STAGED
 #define TC_CM_SLOTS_P_STAGED 8
 #endif
+#ifndef TC_DYN
+#define TC_DYN 2           // > 0: the last TC_DYN rounds of workloads are claimed dynamically; 0: static
+#endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
 #endif
+constexpr int kDynQ = 32;                // dynamic-schedule claim queues per launch
 constexpr int kThreads = TC_THREADS;     // threads per CTA of the classic kernel (one CTA per SM)
 constexpr int kWarps = kThreads / 32;
 
@@ -72,6 +76,7 @@ struct TileArgs {
     const int32_t* split;     // [n_split][3]
     float* partials;          // [n_chunks]
     int32_t* counters;        // [n_split], zero between launches
+    uint32_t* sched;          // [kDynQ + 1]: claim queues, CTAs done; zero between launches
 };
 
 // Slot loads: SMEM = false streams from global memory with evict-first (ld.global.cs); SMEM = true
@@ -375,6 +380,54 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * kWarps;
+#if TC_DYN
+    // Hybrid schedule: all but the last two rounds of workloads are dealt round robin (warp gw
+    // takes gw, gw + G, ...; their slots are bulk-prefetched into L2 two workloads ahead); the
+    // last rounds are claimed from the launch's counter, so the launch ends within about one
+    // workload of its last claim whatever the mix of workload costs.  The claim is issued a whole
+    // workload before its result is needed.  The last warp out resets the counters for the next
+    // launch on the stream.
+    const int64_t n_wl = a.wl_end - a.wl_begin;
+    const int64_t rounds = n_wl / G;
+    // launches of fewer than four rounds stay fully dealt (measured: claiming there loses the
+    // two-ahead L2 prefetch and costs more than the imbalance it removes)
+    const int64_t s_end = rounds >= 4 && rounds > TC_DYN ? (rounds - TC_DYN) * G : n_wl;
+    // the dealt sequence gw, gw + G, ... runs through the first dynamic round (s_end + gw)
+    const int64_t dealt_end = s_end + G < n_wl ? s_end + G : n_wl;
+    if (lane == 0) {
+        for (int q = 0; q < kPrefetchAhead; ++q) {
+            const int64_t jn = gw + q * G;
+            if (jn < dealt_end) prefetch_workload<VALUED>(a, a.wl_begin + jn);
+        }
+    }
+    for (int64_t j = gw; j < s_end; j += G) {
+        const WlDesc d = load_desc(a.desc + a.wl_begin + j);
+        const int64_t jn = j + (int64_t)kPrefetchAhead * G;
+        if (lane == 0 && jn < dealt_end) prefetch_workload<VALUED>(a, a.wl_begin + jn);
+        run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
+    }
+    // dynamic rounds: the first workload is still dealt (no burst of claims at the boundary);
+    // warps that finish early claim the rest
+    // kDynQ queues (queue q holds s_end + G + q + kDynQ*i) spread the claims over as many
+    // addresses: same-address atomics serialise at one L2 slice
+    const int q = (int)(gw % kDynQ);
+    int64_t jc = s_end + gw;
+    while (jc < n_wl) {
+        const WlDesc d = load_desc(a.desc + a.wl_begin + jc);
+        int64_t jf = 0;
+        if (lane == 0) jf = s_end + G + q + (int64_t)kDynQ * atomicAdd(a.sched + q, 1u);   // used after the workload
+        run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
+        if (lane == 0 && jf < n_wl) prefetch_workload<VALUED>(a, a.wl_begin + jf);   // its later batches hit L2
+        jc = __shfl_sync(0xffffffffu, jf, 0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.sched + kDynQ, 1u) == gridDim.x - 1u)
+            for (int i = 0; i <= kDynQ; ++i) a.sched[i] = 0u;
+    }
+    (void)gw; (void)G;
+#else
     // the warp's first workloads: prefetch their slots into L2 (bulk, asynchronous)
     if (lane == 0) {
         for (int q = 0; q < kPrefetchAhead; ++q) {
@@ -389,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         if (lane == 0 && jn < a.wl_end) prefetch_workload<VALUED>(a, jn);
         run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
     }
+#endif
     epi.end();
 }
 

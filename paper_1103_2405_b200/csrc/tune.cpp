@@ -44,6 +44,7 @@ struct PerfTable {
     double launch_us = 3.0;         // per tile launch gap
     double stage_GBps = 6000.0;     // chip-wide L2 -> shared memory staging bandwidth
     double rmw_GBps = 4000.0;       // y read-modify-write of accumulating rows
+    double tail_frac = 0.0;         // launch tail: this fraction of one workload's duration under load
     int max_act_warp = 148 * 32;
     bool loaded = false;
     std::string source = "built-in";
@@ -104,6 +105,7 @@ static bool parse_table(const std::string& text, PerfTable& T) {
     if (num_after("launch_us", v)) T.launch_us = v;
     if (num_after("stage_GBps", v)) T.stage_GBps = v;
     if (num_after("rmw_GBps", v)) T.rmw_GBps = v;
+    if (num_after("tail_frac", v)) T.tail_frac = v;
     if (num_after("max_act_warp", v)) T.max_act_warp = (int)v;
     size_t p = text.find("\"entries\"");
     if (p == std::string::npos) return false;
@@ -190,10 +192,12 @@ static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int6
                       bool split, int ell_h, int cached, bool valued, const PerfTable& T,
                       int64_t* n_workloads = nullptr) {
     const int64_t M = std::max(1, T.max_act_warp);      // MAX_ACT_WARP (Eq. 1)
-    double total = 0.0, P = 0.0, S = 0.0;
+    double total = 0.0, P = 0.0, S = 0.0, P_all = 0.0;
     int64_t cnt = 0, nw = 0;
     auto add = [&](int kind, int64_t w, int64_t h, int64_t slots) {   // Alg. 3 lines 11-14
-        P += T.lookup(cached, valued, kind, (double)std::max<int64_t>(w, 1), (double)h);
+        const double perf = T.lookup(cached, valued, kind, (double)std::max<int64_t>(w, 1), (double)h);
+        P += perf;
+        P_all += perf;
         S += (double)slots;
         ++cnt; ++nw;
         if (cnt == M) { total += S / (P / (double)cnt); P = S = 0.0; cnt = 0; }   // Eq. 3-5
@@ -232,6 +236,9 @@ static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int6
         }
     }
     if (cnt > 0) total += S / (P / (double)cnt);             // last (partial) wave, R23
+    // B200 term (reading R31): the launch ends when its last workload does; on average the
+    // stragglers add tail_frac of one workload's duration under load, WL / (mean P / MAX_ACT_WARP)
+    if (nw > 0 && T.tail_frac > 0.0) total += T.tail_frac * (double)WL * (double)M / (P_all / (double)nw);
     if (n_workloads) *n_workloads = nw;
     return total;   // seconds
 }

@@ -114,3 +114,25 @@ def test_rwr_batch_parity(opt, gpu):
         assert abs(worst - info["residual"]) < 1e-6
         # a single-query run of the same solver still works after the batch
         s.run(int(qs[0]))
+
+
+def test_config0_c1_pagerank_and_spmv(gpu):
+    """BASELINE configs[0]: R-MAT scale 16 (65,536 vertices, 1M edges), PageRank d = 0.85 to
+    1e-6 L1 and fp32 SpMV, against the oracle at full size."""
+    import torch
+    from paper_1103_2405_b200 import Plan, Solver
+    G = graphgen.make_graph("c1")
+    s = Solver("pagerank", G.n, G.row_ptr, G.col, device=0)
+    info = s.run()
+    assert info["converged"] and info["residual"] < 1e-6
+    p = s.result().astype(np.float64)
+    ref, r = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
+    assert np.abs(p - ref).sum() < L1_BAR
+    ref2, r2 = oracle.pagerank(G.n, G.row_ptr, G.col, tol=1e-6)
+    assert abs(r2.iterations - info["iterations"]) <= 1
+    val = graphgen.edge_values(G.keys)
+    x = graphgen.uniform_f32(G.n, seed=graphgen.SEED_X)
+    plan = Plan(G.n, G.n, G.row_ptr, G.col, val, device=0)
+    y = plan.execute_host(x).astype(np.float64)
+    yref, b = oracle.spmv(G.row_ptr, G.col, val, x)
+    assert (np.abs(y - yref) <= 1e-5 * b + 1e-30).all()

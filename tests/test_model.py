@@ -14,7 +14,7 @@ PERF = {"rm": 1.0e9, "cm": 2.5e9}          # constant per kind: lookup is exact,
 TABLE = dict(version=1, max_act_warp=96, launch_us=3.0, stage_GBps=5000.0, rmw_GBps=2500.0)
 
 
-def write_table(tmp_path):
+def write_table(tmp_path, **extra):
     ent = []
     for cached in (0, 1):
         for valued in (0, 1):
@@ -23,7 +23,7 @@ def write_table(tmp_path):
                     ent.append([cached, valued, 0, w, h, PERF["rm"]])
                     ent.append([cached, valued, 1, w, h, PERF["cm"]])
     path = tmp_path / "table.json"
-    path.write_text(json.dumps(dict(TABLE, entries=ent)))
+    path.write_text(json.dumps(dict(TABLE, entries=ent, **extra)))
     return str(path)
 
 
@@ -42,9 +42,14 @@ def tile_hists(n_rows, n_cols, rp, col, tw, T):
     return [sorted(h.items(), key=lambda kv: -kv[0]) for h in hists]
 
 
-def expected_us(h, WL, t, T, tw, cached, split=True):
+def expected_us(h, WL, t, T, tw, cached, split=True, tail_frac=0.0):
     sec = model_ref.pm_packed(h, WL, lambda k, w, hh: PERF[k], TABLE["max_act_warp"], split=split)
     rows = sum(c for _, c in h)
+    if tail_frac and rows:
+        # reading R31: tail_frac of one workload's duration at the mean per-warp rate
+        kinds = workload_kinds(h, WL)
+        mean_perf = sum(PERF[k] for k in kinds) / len(kinds)
+        sec += tail_frac * WL * TABLE["max_act_warp"] / mean_perf
     us = sec * 1e6
     if rows:
         us += TABLE["launch_us"]
@@ -55,10 +60,29 @@ def expected_us(h, WL, t, T, tw, cached, split=True):
     return us
 
 
-@pytest.mark.parametrize("seed", range(4))
-def test_predicted_time_equals_transcription(seed, tmp_path):
+def workload_kinds(h, WL, ell_h=32):
+    """Kinds of the workloads the packing walk forms (brute force over the expanded rows)."""
+    rows = [length for length, count in h for _ in range(count)]
+    kinds, i = [], 0
+    while i < len(rows):
+        w = rows[i]
+        hq = max(1, WL // max(w, 1))
+        if w > WL:
+            kinds += ["rm"] * (-(-w // WL))
+            i += 1
+        elif w >= hq:
+            kinds.append("rm")
+            i += min(hq, len(rows) - i)
+        else:
+            kinds.append("cm")
+            i += min(-(-hq // ell_h) * ell_h, len(rows) - i)
+    return kinds
+
+
+@pytest.mark.parametrize("seed,tail", [(0, 0.0), (1, 0.0), (2, 0.0), (3, 0.0), (4, 0.5), (5, 0.5)])
+def test_predicted_time_equals_transcription(seed, tail, tmp_path):
     from paper_1103_2405_b200 import Plan
-    table = write_table(tmp_path)
+    table = write_table(tmp_path, tail_frac=tail)
     rng = np.random.default_rng(seed)
     nr, nc = int(rng.integers(200, 800)), int(rng.integers(200, 800))
     rp, col, _ = graphgen.random_csr(nr, nc, int(rng.integers(2000, 20000)), seed=seed, kind="powerlaw", valued=False)
@@ -70,7 +94,7 @@ def test_predicted_time_equals_transcription(seed, tmp_path):
     assert st["perf_table_loaded"]
     hists = tile_hists(nr, nc, rp, col, tw, T)
     for t in range(T + 1):
-        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T)
+        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T, tail_frac=tail)
         assert math.isclose(st["tile_predicted_us"][t], exp, rel_tol=1e-9), (t, st["tile_predicted_us"][t], exp)
 
 
