@@ -165,6 +165,34 @@ def make_graph(config: str, **override) -> Graph:
     return graph_from_keys(config, spec["n"], keys)
 
 
+def dense_csr(n_rows: int, n_cols: int, seed: int = SEED_VAL):
+    """Appendix D's dense case: every entry stored, values U(0,1] from the counter
+    generator.  Returns (row_ptr, col, val)."""
+    rp = np.arange(n_rows + 1, dtype=np.int64) * n_cols
+    col = np.tile(np.arange(n_cols, dtype=np.int32), n_rows)
+    val = uniform_f32(n_rows * n_cols, seed=seed, mode=1)
+    return rp, col, val
+
+
+def banded_csr(n: int, half_band: int, seed: int = SEED_VAL, drop: float = 0.0):
+    """Unstructured-mesh-like banded matrix (Appendix D, FEM-like): row i holds the columns
+    [i - half_band, i + half_band] clipped to [0, n); with drop > 0 each off-diagonal entry is
+    removed with that probability (a ragged band).  Values U(0,1].  Returns (row_ptr, col, val)."""
+    rng = np.random.default_rng(seed)
+    off = np.arange(-half_band, half_band + 1)
+    r = np.repeat(np.arange(n, dtype=np.int64), len(off))
+    c = r + np.tile(off, n)
+    keep = (c >= 0) & (c < n)
+    if drop > 0:
+        keep &= (c == r) | (rng.random(len(c)) >= drop)
+    r, c = r[keep], c[keep]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    rp = np.cumsum(rp)
+    val = uniform_f32(len(c), seed=seed, mode=1)
+    return rp, c.astype(np.int32), val
+
+
 def random_csr(n_rows: int, n_cols: int, nnz: int, seed: int = 7, kind: str = "uniform",
                valued: bool = True, signed: bool = False, alpha: float = 2.0):
     """Small random sparse matrices for parity/format tests (rectangular allowed, duplicates

@@ -55,7 +55,7 @@ typedef struct spmv_solver_s* spmv_solver;
 /* Options of the format builder (Sec. 3.1) and of the auto-tuner (Sec. 3.3).
  * spmv_options_default() fills: tile_width 0 (auto), num_tiles -1 (auto), workload_size -1
  * (auto), workload_sizes NULL, align_rm 8, split_long_rows 1, camping_pad 0, pattern 0,
- * ell_h 32, stage_x 1, perf_table_path NULL. */
+ * ell_h 32, stage_x 1, perf_table_path NULL, orient 0. */
 typedef struct {
     int32_t tile_width;      /* columns per dense tile (paper: 64K, L60); 0 = chosen by the tuner */
     int32_t num_tiles;       /* dense tiles before the remainder; -1 = auto (Alg. 1 + B200 model);
@@ -71,6 +71,10 @@ typedef struct {
     int32_t ell_h;           /* column-major slab height (warp size); must be 32 to execute */
     int32_t stage_x;         /* 1: dense tiles stage their x segment in shared memory */
     const char* perf_table_path; /* JSON offline table (Sec. 3.3); NULL = built-in B200 table */
+    int32_t orient;          /* workload orientation (§8(f) f2 ablations; the model covers the
+                                single-format cases): 0 = composite (Alg. 3: row major iff
+                                w >= h), 1 = row major only (CSR-vector), 2 = column major only (ELL).
+                                Rows of length 0 and split chunks are unaffected. */
 } spmv_options;
 
 void spmv_options_default(spmv_options* opt);

@@ -71,7 +71,7 @@ def paper_tile_count(collen_sorted: np.ndarray, n_cols: int, tw: int) -> int:
 
 
 def build(n_rows, n_cols, row_ptr, col, val, tile_width, num_tiles, workload_sizes,
-          align_rm=8, split_long_rows=True, camping_pad=False, ell_h=32) -> Layout:
+          align_rm=8, split_long_rows=True, camping_pad=False, ell_h=32, orient=0) -> Layout:
     """Build the layout from explicit parameters (the autotuner is not involved here).
     workload_sizes: list of num_tiles + 1 ints (the last is the remainder tile's WL)."""
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
@@ -178,7 +178,9 @@ def build(n_rows, n_cols, row_ptr, col, val, tile_width, num_tiles, workload_siz
                     camp()
                 i += 1
                 continue
-            if w >= hq:                            # row major, CSR-vector style
+            # Alg. 3's rule (row major iff w >= h); orient 1 / 2 force one format for the
+            # single-format special cases the model covers, zero-length rows excepted
+            if (w > 0) if orient == 1 else (False if orient == 2 else w >= hq):   # row major
                 h = min(hq, len(rows) - i)
                 wp = _roundup(w, align_rm)
                 emit(cur_off, len(row_id), wp, h, KIND_RM, 4, -1, 0)

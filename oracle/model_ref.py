@@ -79,7 +79,7 @@ def _rup(a, b):
     return (a + b - 1) // b * b
 
 
-def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32):
+def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32, orient=0):
     """B200 reading of Alg. 3: the same wave model (Eq. 1-5) charged over
     the workloads the format actually builds (the packing of Solution 3 / format_ref with row
     splitting, R21, and clipping, R13), each looked up at its padded shape.
@@ -107,7 +107,7 @@ def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32):
                 add("rm", wp, 1, wp)
                 c += 1
             i += 1
-        elif w >= hq:
+        elif ((w > 0) if orient == 1 else (False if orient == 2 else w >= hq)):
             h = min(hq, len(rows) - i)
             wp = _rup(w, align)
             add("rm", wp, h, h * wp)

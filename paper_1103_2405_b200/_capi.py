@@ -21,7 +21,8 @@ class Options(ctypes.Structure):
     _fields_ = [("tile_width", c_i32), ("num_tiles", c_i32), ("workload_size", c_i32),
                 ("workload_sizes", ctypes.POINTER(c_i32)), ("align_rm", c_i32),
                 ("split_long_rows", c_i32), ("camping_pad", c_i32), ("pattern", c_i32),
-                ("ell_h", c_i32), ("stage_x", c_i32), ("perf_table_path", ctypes.c_char_p)]
+                ("ell_h", c_i32), ("stage_x", c_i32), ("perf_table_path", ctypes.c_char_p),
+                ("orient", c_i32)]
 
 
 class PlanStats(ctypes.Structure):

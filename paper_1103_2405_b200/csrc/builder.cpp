@@ -232,7 +232,7 @@ spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L)
                 ++i;
                 continue;
             }
-            if (w >= hq) {
+            if (row_major(bp.orient, w, hq)) {
                 int64_t h = std::min<int64_t>(hq, nr - i);
                 int64_t wp = roundup(w, align);
                 L.desc.push_back(WlDesc{n_slots, (int32_t)L.row_id.size(), (int32_t)wp, (int32_t)h, KIND_RM, 4, 0, -1, 0});

@@ -72,6 +72,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     auto t0 = std::chrono::steady_clock::now();
     spmv_options opt;
     if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
+    if (opt.orient < 0 || opt.orient > 2) { set_error("orient must be 0, 1 or 2"); return SPMV_EINVAL; }
     if (device >= 0 && (opt.ell_h != 32 || opt.align_rm % 4 != 0)) {
         set_error("device plans need ell_h = 32 and align_rm % 4 == 0"); return SPMV_EINVAL;
     }
@@ -200,7 +201,7 @@ __attribute__((visibility("default"))) void spmv_options_default(spmv_options* o
     std::memset(o, 0, sizeof(*o));
     o->tile_width = 0; o->num_tiles = -1; o->workload_size = -1; o->workload_sizes = nullptr;
     o->align_rm = 8; o->split_long_rows = 1; o->camping_pad = 0; o->pattern = 0; o->ell_h = 32;
-    o->stage_x = 1; o->perf_table_path = nullptr;
+    o->stage_x = 1; o->perf_table_path = nullptr; o->orient = 0;
 }
 
 __attribute__((visibility("default")))

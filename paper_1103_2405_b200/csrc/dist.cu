@@ -135,10 +135,13 @@ struct Dist {
     int P = 1, rank = 0;
     uint8_t* d_half_local = nullptr;         // HITS: half flag per local row
     uint8_t* d_col_half = nullptr;           // HITS: half flag per permuted column (k < nzc)
-    int64_t n_local = 0, S = 0, slot = 0;    // owned rows, slot rows, slot floats (S + partials)
+    int64_t n_local = 0, S = 0, slot = 0;    // owned rows, exchanged rows per slot, slot floats (S + partials)
+    int64_t S_full = 0;                      // owned rows per slot of the one-time result gather
     int64_t nzc = 0;                         // local columns with entries (plan column prefix)
-    std::vector<int64_t> gpos;               // vertex -> position in the gathered buffer
+    std::vector<int64_t> gpos;               // vertex -> position in the gathered buffer (-1: never exchanged)
+    std::vector<int64_t> gpos_full;          // vertex -> position in the result gather
     std::vector<int32_t> owned;              // local row -> vertex
+    std::vector<int64_t> lrow;               // vertex -> local row index on its owner
     int64_t q_local = -1;
     float* d_G = nullptr;                    // gathered buffer: P slots
     int32_t* d_idx = nullptr;                // x'[k] = G[idx[k]] for k < nzc
@@ -175,7 +178,7 @@ __global__ void dist_init(float* p, float* zslot, const float* inv, int64_t n_lo
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += (int64_t)gridDim.x * blockDim.x) {
         float v = rwr ? (i == q_local ? 1.0f : 0.0f) : p0;
         p[i] = v;
-        zslot[i] = v * inv[i];
+        if (inv[i] != 0.0f) zslot[i] = v * inv[i];   // empty columns (inv = 0) are not exchanged
     }
 }
 
@@ -284,12 +287,29 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         std::vector<int64_t> lidx(n);
         int64_t S = 0;
         if ((st = spmv_partition_plan(n, rl.data(), D->P, owner.data(), lidx.data(), &S))) throw st;
-        D->S = (S + 3) / 4 * 4;
+        // Exchange only globally non-empty columns: for PageRank / RWR a column of
+        // the iteration matrix is empty exactly when the vertex has no out-edges (inv = 0), so its
+        // z is never read.  On each rank the non-empty rows come first (ascending id), then the
+        // rest; the exchanged slot holds the first part only.  HITS exchanges every row.
+        std::vector<char> col_ne(n, algo == SPMV_ALGO_HITS ? 1 : 0);
+        if (algo != SPMV_ALGO_HITS)
+            for (int64_t u = 0; u < n; ++u) col_ne[u] = len[u] != 0;
+        std::vector<int64_t> cnt_ne(D->P, 0), cnt_all(D->P, 0);
+        for (int64_t i = 0; i < n; ++i) { cnt_ne[owner[i]] += col_ne[i]; cnt_all[owner[i]]++; }
+        std::vector<int64_t> next_ne(D->P, 0), next_e(cnt_ne);
+        D->lrow.resize(n);
+        for (int64_t i = 0; i < n; ++i) D->lrow[i] = col_ne[i] ? next_ne[owner[i]]++ : next_e[owner[i]]++;
+        const int64_t S_ex = n ? *std::max_element(cnt_ne.begin(), cnt_ne.end()) : 0;
+        D->S = (S_ex + 3) / 4 * 4;
         D->slot = D->S + kPartialFloats;
+        D->S_full = std::max<int64_t>(S, 1);
         D->gpos.resize(n);
+        D->gpos_full.resize(n);
+        D->owned.assign(cnt_all[D->rank], 0);
         for (int64_t i = 0; i < n; ++i) {
-            D->gpos[i] = (int64_t)owner[i] * D->slot + lidx[i];
-            if (owner[i] == D->rank) D->owned.push_back((int32_t)i);
+            D->gpos[i] = col_ne[i] ? (int64_t)owner[i] * D->slot + D->lrow[i] : -1;
+            D->gpos_full[i] = (int64_t)owner[i] * D->S_full + D->lrow[i];
+            if (owner[i] == D->rank) D->owned[D->lrow[i]] = (int32_t)i;
         }
         D->n_local = (int64_t)D->owned.size();
         // local rows (ascending vertex id = local index order), original column ids
@@ -310,7 +330,10 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         spmv_plan_s* p = s->plan;
         // the plan's columns are ordered by local length: the first nzc have entries
         std::vector<int32_t> idx(D->nzc);
-        for (int64_t k = 0; k < D->nzc; ++k) idx[k] = (int32_t)D->gpos[p->perm[k]];
+        for (int64_t k = 0; k < D->nzc; ++k) {
+            idx[k] = (int32_t)D->gpos[p->perm[k]];
+            if (idx[k] < 0) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
+        }
         std::vector<float> inv(std::max<int64_t>(D->n_local, 1), 0.0f);
         int64_t n_dangling = 0;
         for (int64_t u = 0; u < n; ++u) n_dangling += (len[u] == 0);
@@ -396,7 +419,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     const int rwr = s->algo == SPMV_ALGO_RWR;
     const int hitsa = s->algo == SPMV_ALGO_HITS;
     D->q_local = -1;
-    if (rwr && (int32_t)(D->gpos[query] / D->slot) == D->rank) D->q_local = D->gpos[query] % D->slot;
+    if (rwr && D->lrow[query] < D->n_local && D->owned[D->lrow[query]] == (int32_t)query) D->q_local = D->lrow[query];
     Ctrl c{};
     const double n = (double)s->n;
     c.c = s->it.c; c.tol = s->it.tol; c.max_iter = s->it.max_iter; c.fixed_iters = s->it.fixed_iters;
@@ -489,20 +512,25 @@ spmv_status solver_result_dist(spmv_solver s, float* out0, float* out1) {
     Dist* D = static_cast<Dist*>(s->dist);
     cudaSetDevice(s->device);
     cudaStream_t st = s->own_stream;
-    float* slot = D->d_G + (int64_t)D->rank * D->slot;
+    // one-time gather of every owned row (the iteration exchange skips empty columns)
+    float* d_R = nullptr;
+    cudaError_t e = cudaMalloc(&d_R, (size_t)D->P * D->S_full * sizeof(float));
+    if (e) return cuda_status(e, "result buffer");
+    float* slot = d_R + (int64_t)D->rank * D->S_full;
     if (s->algo == SPMV_ALGO_HITS)
         cudaMemcpyAsync(slot, s->d_p, D->n_local * sizeof(float), cudaMemcpyDeviceToDevice, st);
     else
         gather_rows<<<s->plan->sm_count * 4, 256, 0, st>>>(s->d_p_e, s->d_fpos, slot, D->n_local);
-    spmv_status ss = allgather(s->comm, D->d_G, D->slot, st);
-    if (ss) return ss;
-    std::vector<float> G((size_t)D->P * D->slot);
-    cudaError_t e = cudaMemcpyAsync(G.data(), D->d_G, G.size() * sizeof(float), cudaMemcpyDeviceToHost, st);
+    spmv_status ss = allgather(s->comm, d_R, D->S_full, st);
+    if (ss) { cudaFree(d_R); return ss; }
+    std::vector<float> G((size_t)D->P * D->S_full);
+    e = cudaMemcpyAsync(G.data(), d_R, G.size() * sizeof(float), cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaStreamSynchronize(st);
+    cudaFree(d_R);
     if (e) return cuda_status(e, "result");
-    for (int64_t u = 0; u < s->n; ++u) out0[u] = G[D->gpos[u]];
+    for (int64_t u = 0; u < s->n; ++u) out0[u] = G[D->gpos_full[u]];
     if (s->algo == SPMV_ALGO_HITS)
-        for (int64_t u = 0; u < s->n; ++u) out1[u] = G[D->gpos[s->n + u]];
+        for (int64_t u = 0; u < s->n; ++u) out1[u] = G[D->gpos_full[s->n + u]];
     return SPMV_OK;
 }
 

@@ -115,8 +115,10 @@ struct EpiAffine {
         if (rwr && (int32_t)r == q) pn += 1.0f - c;
         res += fabs((double)pn - (double)pre.p_old);
         p[slot(ent, e)] = pn;
-        z_next[r] = pn * pre.inv;
-        if (pre.inv == 0.0f) dm += (double)pn;
+        // a vertex without out-edges is an empty column of the iteration matrix: its z is never
+        // read (and, row-partitioned, has no place in the exchanged slot)
+        if (pre.inv != 0.0f) z_next[r] = pn * pre.inv;
+        else dm += (double)pn;
     }
     __device__ __forceinline__ void end() {
         double v[2] = {res, dm};

@@ -73,7 +73,13 @@ struct BuildParams {
     bool split = true;
     bool camping = false;
     int32_t ell_h = 32;
+    int32_t orient = 0;               // 0 composite, 1 row major only, 2 column major only
 };
+
+// Alg. 3's orientation rule (row major iff w >= h), or a forced single format (f2 ablations).
+inline bool row_major(int32_t orient, int64_t w, int64_t hq) {
+    return orient == 1 ? w > 0 : (orient == 2 ? false : w >= hq);
+}
 
 // errors are reported through set_error() + status
 void set_error(const std::string& msg);

@@ -54,6 +54,15 @@ namespace tc {
 #ifndef TC_DYN
 #define TC_DYN 2           // > 0: the last TC_DYN rounds of workloads are claimed dynamically; 0: static
 #endif
+#ifndef TC_PF_AHEAD
+#define TC_PF_AHEAD 2      // workloads of each warp bulk-prefetched into L2 ahead of use
+#endif
+#ifndef TC_PF_POLICY
+#define TC_PF_POLICY 0     // 1: prefetched slot lines enter L2 evict-first
+#endif
+#ifndef TC_X_POLICY
+#define TC_X_POLICY 0      // 1: x gathers carry an L2 evict-last policy (x stays resident)
+#endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
 #endif
@@ -118,10 +127,18 @@ struct XSrc {
     int32_t width;
     int32_t hot;
     int32_t prefix;
+    uint64_t pol = 0;   // TC_X_POLICY: L2 evict-last policy for the gathers
     __device__ __forceinline__ float operator()(int32_t c) const {
         if (c == width) return 0.0f;                  // padding slot (sentinel, reading R16)
         if (STAGED) return s[c];
         if (c < prefix) return s[c];
+#if TC_X_POLICY
+        {
+            float v;
+            asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
+            return v;
+        }
+#endif
         if (hot <= 0) return __ldg(g + c);
         float v;
         if (c < hot) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
@@ -344,15 +361,21 @@ __device__ __forceinline__ void run_workload(const TileArgs& a, const WlDesc& d,
     else dispatch_cm<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
 }
 
-constexpr int kPrefetchAhead = 2;
+constexpr int kPrefetchAhead = TC_PF_AHEAD;
 
 template <bool VALUED>
 __device__ __forceinline__ void prefetch_workload(const TileArgs& a, int64_t j) {
     const WlDesc d = load_desc(a.desc + j);
     const uint32_t bytes = (uint32_t)((int64_t)d.h * d.w * 4 + 15) & ~15u;
     if (bytes == 0) return;
+#if TC_PF_POLICY
+    const uint64_t pol = policy_evict_first();
+    bulk_prefetch_l2_hint(a.col + d.off, bytes, pol);
+    if (VALUED) bulk_prefetch_l2_hint(a.val + d.off, bytes, pol);
+#else
     bulk_prefetch_l2(a.col + d.off, bytes);
     if (VALUED) bulk_prefetch_l2(a.val + d.off, bytes);
+#endif
 }
 
 template <bool STAGED, bool VALUED, class Epi>
@@ -377,6 +400,9 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         __syncthreads();
     }
     XSrc<STAGED> x{a.x, xs, a.width, a.hot, STAGED ? 0 : a.prefix};
+#if TC_X_POLICY
+    x.pol = policy_evict_last();
+#endif
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * kWarps;

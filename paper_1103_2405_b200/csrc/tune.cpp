@@ -190,7 +190,7 @@ static const PerfTable& table_for(const char* path_opt) {
 // rules as pack_layout and charges every workload to its wave.
 static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int64_t WL, int align,
                       bool split, int ell_h, int cached, bool valued, const PerfTable& T,
-                      int64_t* n_workloads = nullptr) {
+                      int64_t* n_workloads = nullptr, int32_t orient = 0) {
     const int64_t M = std::max(1, T.max_act_warp);      // MAX_ACT_WARP (Eq. 1)
     double total = 0.0, P = 0.0, S = 0.0, P_all = 0.0;
     int64_t cnt = 0, nw = 0;
@@ -224,7 +224,7 @@ static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int6
                 add(KIND_RM, wp, 1, wp);
             }
             advance(1);
-        } else if (w >= hq) {                                // row major
+        } else if (row_major(orient, w, hq)) {               // row major
             const int64_t h = std::min<int64_t>(hq, remaining), wp = rup(w, align);
             add(KIND_RM, wp, h, h * wp);
             advance(h);
@@ -260,7 +260,7 @@ static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist,
     }
     opt_t = INFINITY; opt_wl = (int32_t)cand[0];
     for (int64_t c : cand) {
-        double t = pm_tile(hist, c, bp.align_rm, bp.split, bp.ell_h, cached, valued, T);
+        double t = pm_tile(hist, c, bp.align_rm, bp.split, bp.ell_h, cached, valued, T, nullptr, bp.orient);
         if (t < opt_t) { opt_t = t; opt_wl = (int32_t)c; }
     }
 }
@@ -282,7 +282,7 @@ static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildPa
         else if (opt.workload_size > 0) wl = opt.workload_size;
         if (opt.workload_sizes || opt.workload_size > 0) {
             BuildParams b = base; b.wl.assign(1, wl);
-            sec = pm_tile(hist[t], wl, b.align_rm, b.split, b.ell_h, mode, valued, tab);
+            sec = pm_tile(hist[t], wl, b.align_rm, b.split, b.ell_h, mode, valued, tab, nullptr, b.orient);
         } else {
             partition_tile(hist[t], base, mode, valued, tab, wl, sec);
         }
@@ -307,6 +307,7 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
     bp.split = opt.split_long_rows != 0;
     bp.camping = opt.camping_pad != 0;
     bp.ell_h = opt.ell_h;
+    bp.orient = opt.orient;
     PerfTable tab = table_for(opt.perf_table_path);
     tab.max_act_warp = std::max(1, (int)((int64_t)tab.max_act_warp * sm_count / 148));
     if (opt.perf_table_path && !tab.loaded) { set_error("performance table unreadable"); return SPMV_ETABLE; }

@@ -28,13 +28,13 @@ def test_library_exports_every_header_symbol():
     assert _capi.lib().spmv_version().startswith(b"tcspmv")
 
 
-def build_both(nr, nc, rp, col, val, tw, T, wls, align=8, split=True, camping=False, ell_h=32):
+def build_both(nr, nc, rp, col, val, tw, T, wls, align=8, split=True, camping=False, ell_h=32, orient=0):
     from paper_1103_2405_b200 import Plan
     ref = format_ref.build(nr, nc, rp, col, val, tw, T, wls, align_rm=align, split_long_rows=split,
-                           camping_pad=camping, ell_h=ell_h)
+                           camping_pad=camping, ell_h=ell_h, orient=orient)
     p = Plan(nr, nc, rp, col, val, device=-1, tile_width=tw, num_tiles=T, workload_sizes=wls,
              align_rm=align, split_long_rows=int(split), camping_pad=int(camping), ell_h=ell_h,
-             pattern=int(val is None))
+             pattern=int(val is None), orient=orient)
     return ref, p
 
 
@@ -86,6 +86,28 @@ def test_random_bit_exact(seed):
     exp_v = np.ones(len(col), np.float32) if val is None else val
     exp = sorted(zip(np.repeat(np.arange(nr), np.diff(rp)).tolist(), col.tolist(), exp_v.tolist()))
     assert got == exp
+
+
+@pytest.mark.parametrize("orient", [1, 2])
+@pytest.mark.parametrize("seed", range(4))
+def test_single_format_orientations_bit_exact(orient, seed):
+    """f2 ablation layouts: row major only (CSR-vector) and column major only (ELL)."""
+    rng = np.random.default_rng(2000 + seed)
+    nr, nc = int(rng.integers(50, 500)), int(rng.integers(50, 500))
+    rp, col, val = graphgen.random_csr(nr, nc, int(rng.integers(500, 6000)), seed=seed, kind="powerlaw",
+                                       valued=seed % 2 == 0)
+    tw = int(rng.integers(8, 64))
+    T = int(rng.integers(0, 3))
+    wls = [int(rng.integers(16, 300)) for _ in range(T + 1)]
+    ref, p = build_both(nr, nc, rp, col, val, tw, T, wls, orient=orient)
+    assert_same(ref, p)
+    kind, w = ref.desc["kind"], ref.desc["w"]
+    if orient == 1:      # only zero-length rows stay column major
+        assert (w[kind == format_ref.KIND_CM] == 0).all()
+    else:
+        assert not (kind == format_ref.KIND_RM).any()
+    r, c, v = p.to_coo()
+    assert len(r) == len(col)
 
 
 def test_graph_bit_exact_t_small():

@@ -41,6 +41,11 @@ CASES = [
     (2000, 2000, 50000, "powerlaw", True, False, dict(tile_width=512, num_tiles=2, workload_size=96, camping_pad=1)),
     (3000, 3000, 90000, "powerlaw", True, False, dict(num_tiles=0, split_long_rows=0)),
     (3000, 3000, 90000, "powerlaw", True, False, dict()),
+    # f2 single-format layouts: CSR-vector (row major only) and ELL (column major only)
+    (3000, 3000, 90000, "powerlaw", True, True, dict(orient=1)),
+    (3000, 3000, 90000, "powerlaw", False, False, dict(orient=1, tile_width=256, num_tiles=2, workload_size=256)),
+    (3000, 3000, 90000, "powerlaw", True, True, dict(orient=2)),
+    (3000, 3000, 90000, "powerlaw", False, False, dict(orient=2, tile_width=256, num_tiles=2, workload_size=512)),
 ]
 
 
@@ -132,3 +137,23 @@ def test_full_size_c2_sampled_rows(gpu):
     y2 = torch.empty(G.n, device="cuda")
     p.execute(xt, y2)
     assert y2.cpu().numpy().tobytes() == y.tobytes()
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048), (300, 5000), (5000, 40)])
+def test_dense_matrices(shape, gpu):
+    """Appendix D dense case (§8(f) f4): every row is full; rows longer than WL split."""
+    nr, nc = shape
+    rp, col, val = graphgen.dense_csr(nr, nc)
+    x = graphgen.uniform_f32(nc, seed=graphgen.SEED_X)
+    _, y = run_plan(nr, nc, rp, col, val, x)
+    check(y, rp, col, val, x)
+
+
+@pytest.mark.parametrize("half_band,drop", [(13, 0.0), (4, 0.3), (40, 0.5)])
+def test_banded_matrices(half_band, drop, gpu):
+    """FEM-like banded matrices (§8(f) f4), with and without a ragged band."""
+    n = 50_000
+    rp, col, val = graphgen.banded_csr(n, half_band, drop=drop)
+    x = graphgen.uniform_f32(n, seed=graphgen.SEED_X, mode=2)
+    _, y = run_plan(n, n, rp, col, val, x)
+    check(y, rp, col, val, x)

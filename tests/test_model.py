@@ -42,12 +42,12 @@ def tile_hists(n_rows, n_cols, rp, col, tw, T):
     return [sorted(h.items(), key=lambda kv: -kv[0]) for h in hists]
 
 
-def expected_us(h, WL, t, T, tw, cached, split=True, tail_frac=0.0):
-    sec = model_ref.pm_packed(h, WL, lambda k, w, hh: PERF[k], TABLE["max_act_warp"], split=split)
+def expected_us(h, WL, t, T, tw, cached, split=True, tail_frac=0.0, orient=0):
+    sec = model_ref.pm_packed(h, WL, lambda k, w, hh: PERF[k], TABLE["max_act_warp"], split=split, orient=orient)
     rows = sum(c for _, c in h)
     if tail_frac and rows:
         # reading R31: tail_frac of one workload's duration at the mean per-warp rate
-        kinds = workload_kinds(h, WL)
+        kinds = workload_kinds(h, WL, orient=orient)
         mean_perf = sum(PERF[k] for k in kinds) / len(kinds)
         sec += tail_frac * WL * TABLE["max_act_warp"] / mean_perf
     us = sec * 1e6
@@ -60,7 +60,7 @@ def expected_us(h, WL, t, T, tw, cached, split=True, tail_frac=0.0):
     return us
 
 
-def workload_kinds(h, WL, ell_h=32):
+def workload_kinds(h, WL, ell_h=32, orient=0):
     """Kinds of the workloads the packing walk forms (brute force over the expanded rows)."""
     rows = [length for length, count in h for _ in range(count)]
     kinds, i = [], 0
@@ -70,7 +70,7 @@ def workload_kinds(h, WL, ell_h=32):
         if w > WL:
             kinds += ["rm"] * (-(-w // WL))
             i += 1
-        elif w >= hq:
+        elif (w > 0) if orient == 1 else (orient == 0 and w >= hq):
             kinds.append("rm")
             i += min(hq, len(rows) - i)
         else:
@@ -79,8 +79,9 @@ def workload_kinds(h, WL, ell_h=32):
     return kinds
 
 
-@pytest.mark.parametrize("seed,tail", [(0, 0.0), (1, 0.0), (2, 0.0), (3, 0.0), (4, 0.5), (5, 0.5)])
-def test_predicted_time_equals_transcription(seed, tail, tmp_path):
+@pytest.mark.parametrize("seed,tail,orient", [(0, 0.0, 0), (1, 0.0, 0), (2, 0.0, 0), (3, 0.0, 0), (4, 0.5, 0),
+                                              (5, 0.5, 0), (6, 0.0, 1), (7, 0.5, 2)])
+def test_predicted_time_equals_transcription(seed, tail, orient, tmp_path):
     from paper_1103_2405_b200 import Plan
     table = write_table(tmp_path, tail_frac=tail)
     rng = np.random.default_rng(seed)
@@ -89,12 +90,12 @@ def test_predicted_time_equals_transcription(seed, tail, tmp_path):
     tw, T = 64, 3
     wls = [int(x) for x in rng.choice([32, 64, 128, 256], size=T + 1)]
     p = Plan(nr, nc, rp, col, None, device=-1, tile_width=tw, num_tiles=T, workload_sizes=wls,
-             perf_table_path=table)
+             perf_table_path=table, orient=orient)
     st = p.stats()
     assert st["perf_table_loaded"]
     hists = tile_hists(nr, nc, rp, col, tw, T)
     for t in range(T + 1):
-        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T, tail_frac=tail)
+        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T, tail_frac=tail, orient=orient)
         assert math.isclose(st["tile_predicted_us"][t], exp, rel_tol=1e-9), (t, st["tile_predicted_us"][t], exp)
 
 

@@ -82,3 +82,81 @@ def test_gloo_exchange_protocol(world, tmp_path):
     for r in range(world):
         y = np.load(tmp_path / f"y{r}.npy")
         assert np.array_equal(y, ref)          # every rank holds the identical full vector
+
+
+def _worker_pagerank(rank, world, port, result_dir, iters):
+    """The row-partitioned PageRank protocol of csrc/dist.cu in fp64: bitonic ownership; on each
+    rank the rows whose column is non-empty (out-degree > 0) first, so the exchanged slot carries
+    only those z values plus two fp64 partials (sum |dp|, dangling mass) summed in rank order."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1103_2405_b200 import partition_plan
+    G = graphgen.make_graph("t_small")
+    n, c = G.n, 0.85
+    outdeg = np.diff(G.row_ptr)
+    rp, col = graphgen.keys_to_csr(G.keys, n, transpose=True)       # M = A^T
+    owner, _, _ = partition_plan(np.diff(rp), world)
+    col_ne = outdeg > 0
+    lrow = np.zeros(n, np.int64)
+    cnt_ne = np.zeros(world, np.int64)
+    for r in range(world):
+        own = np.nonzero(owner == r)[0]
+        ne, em = own[col_ne[own]], own[~col_ne[own]]
+        lrow[ne] = np.arange(len(ne))
+        lrow[em] = len(ne) + np.arange(len(em))
+        cnt_ne[r] = len(ne)
+    S = int(cnt_ne.max())
+    slot = S + 2
+    mine = np.nonzero(owner == rank)[0]
+    mine = mine[np.argsort(lrow[mine])]
+    sub_rp = np.concatenate([[0], np.cumsum(np.diff(rp)[mine])]).astype(np.int64)
+    sub_col = np.concatenate([col[rp[r]:rp[r + 1]] for r in mine]) if len(mine) else np.zeros(0, np.int32)
+    inv = np.where(outdeg[mine] > 0, 1.0 / np.maximum(outdeg[mine], 1), 0.0)
+    gpos = np.where(col_ne, owner.astype(np.int64) * slot + lrow, -1)
+    p = np.full(len(mine), 1.0 / n)
+
+    def exchange(p, partials):
+        buf = np.zeros(slot)
+        k = int(cnt_ne[rank])
+        buf[:k] = (p * inv)[:k]
+        assert not (p * inv)[k:].any()                 # empty columns carry nothing
+        buf[S:] = partials
+        parts = [torch.zeros(slot, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(buf))
+        Gb = torch.cat(parts).numpy()
+        z = np.where(gpos >= 0, Gb[np.maximum(gpos, 0)], 0.0)
+        tot = sum(Gb[r * slot + S: r * slot + S + 2] for r in range(world))   # rank order
+        return z, tot
+
+    dm0 = float(p[outdeg[mine] == 0].sum())
+    z, tot = exchange(p, [0.0, dm0])
+    D = tot[1]
+    rows_of = np.repeat(np.arange(len(mine)), np.diff(sub_rp))
+    for _ in range(iters):
+        y = np.bincount(rows_of, weights=z[sub_col], minlength=len(mine))     # fp64 local SpMV
+        pn = c * (y + D / n) + (1 - c) / n
+        part = [float(np.abs(pn - p).sum()), float(pn[outdeg[mine] == 0].sum())]
+        p = pn
+        z, tot = exchange(p, part)
+        D = tot[1]
+    # result gather (full slots)
+    full = np.zeros(n)
+    parts = [None] * world
+    dist.all_gather_object(parts, (mine.tolist(), p.tolist()))
+    for rows, vals in parts:
+        full[rows] = vals
+    np.save(os.path.join(result_dir, f"p{rank}.npy"), full)
+    dist.destroy_process_group()
+
+
+def test_gloo_pagerank_skip_empty_columns(tmp_path):
+    world, iters = 2, 12
+    port = _free_port()
+    mp.spawn(_worker_pagerank, args=(world, port, str(tmp_path), iters), nprocs=world, join=True)
+    G = graphgen.make_graph("t_small")
+    ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=iters)
+    for r in range(world):
+        p = np.load(tmp_path / f"p{r}.npy")
+        assert np.abs(p - ref).sum() < 1e-12
