@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "epilogues.cuh"
@@ -196,6 +198,8 @@ __global__ void spmm_init(float* R, float* Z, const float* inv, const int32_t* q
 using namespace tc;
 
 struct BatchState {
+    spmv_plan_s* plan = nullptr;        // the batch's own tiling of the iteration matrix
+    std::vector<int32_t> tiles;         // non-empty tiles of `plan`
     float *R = nullptr, *Z[2] = {nullptr, nullptr}, *Y = nullptr, *partials = nullptr;
     int32_t* q = nullptr;
     double *slots = nullptr, *res = nullptr;
@@ -209,7 +213,7 @@ struct BatchState {
 
 static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int parity, int32_t slot_base,
                             int32_t total_slots, bool is_last, cudaGraphConditionalHandle cond) {
-    spmv_plan_s* p = s->plan;
+    spmv_plan_s* p = B->plan;
     const TileInfo& ti = p->tiles[t];
     BatchArgs a{};
     a.desc = p->d_desc; a.wl_begin = ti.wl_begin; a.wl_end = ti.wl_end;
@@ -222,16 +226,65 @@ static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int pari
     return a;
 }
 
+// Tiling for the batch (Solution 1, where it pays on B200): a gathered x row is 128
+// bytes here, so the hub columns' rows are worth keeping in L2 -- one dense tile whose Z segment
+// takes about 40 % of L2, then the remainder.  The single-query plan stays untiled (4-byte gathers
+// are request-bound).  Built from the solver plan's layout (identical matrix; the
+// column order is the same length order, so the plan permutation stays the identity).
+static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
+    spmv_plan_s* p = s->plan;
+    int64_t tw = 0;
+    int32_t T = 0;
+    {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s->device);
+        tw = std::max<int64_t>(4096, (int64_t)(0.4 * l2) / (kQP * 4)) / 4096 * 4096;
+        if (const char* e = std::getenv("TCSPMV_BATCH_TW")) tw = std::atoll(e);
+        T = p->n_cols > tw ? 1 : 0;
+        if (const char* e = std::getenv("TCSPMV_BATCH_TILES")) T = std::atoi(e);
+        T = (int32_t)std::min<int64_t>(T, (p->n_cols + tw - 1) / std::max<int64_t>(tw, 1));
+    }
+    std::vector<int32_t> rows(std::max<int64_t>(p->nnz, 1)), cols(std::max<int64_t>(p->nnz, 1));
+    spmv_status st = spmv_plan_to_coo(p, rows.data(), cols.data(), nullptr);
+    if (st) return st;
+    std::vector<int64_t> rp(p->n_rows + 1, 0);
+    for (int64_t k = 0; k < p->nnz; ++k) rp[rows[k] + 1]++;
+    for (int64_t i = 0; i < p->n_rows; ++i) rp[i + 1] += rp[i];
+    std::vector<int32_t> col(std::max<int64_t>(p->nnz, 1));
+    {
+        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+        for (int64_t k = 0; k < p->nnz; ++k) col[fill[rows[k]]++] = cols[k];
+    }
+    rows = {}; cols = {};
+    spmv_options opt = p->opt;
+    opt.pattern = 1; opt.workload_sizes = nullptr; opt.perf_table_path = nullptr;
+    opt.tile_width = (int32_t)std::min<int64_t>(tw, INT32_MAX);
+    opt.num_tiles = T;
+    opt.stage_x = 0;
+    if (opt.workload_size <= 0) opt.workload_size = p->opt.workload_size > 0 ? p->opt.workload_size : 1024;
+    st = create_plan(p->n_rows, p->n_cols, p->nnz, rp.data(), col.data(), nullptr, &opt, s->device, &B->plan);
+    if (st) return st;
+    for (int64_t k = 0; k < p->n_cols; ++k)
+        if (B->plan->perm[k] != (int32_t)k) { set_error("internal: batch plan permutation"); return SPMV_EINVAL; }
+    for (int32_t t = 0; t <= B->plan->num_tiles; ++t)
+        if (B->plan->tiles[t].wl_end > B->plan->tiles[t].wl_begin) B->tiles.push_back(t);
+    // the solver plan's host layout copy was only needed for the decode
+    p->L.desc = {}; p->L.row_id = {}; p->L.slot_col = {}; p->L.slot_val = {}; p->L.split = {};
+    p->host_valid = false;
+    return SPMV_OK;
+}
+
 static cudaError_t enqueue_batch_iteration(spmv_solver_s* s, BatchState* B, int parity, cudaStream_t st,
                                            cudaGraphConditionalHandle cond) {
-    const size_t nu = s->tiles_used.size();
+    const size_t nu = B->tiles.size();
+    const int sms = B->plan->sm_count;
     int32_t total = 0;
-    for (size_t i = 0; i < nu; ++i) total += s->plan->sm_count;
+    for (size_t i = 0; i < nu; ++i) total += sms;
     int32_t base = 0;
     for (size_t i = 0; i < nu; ++i) {
-        BatchArgs a = batch_args(s, B, s->tiles_used[i], parity, base, total, i + 1 == nu, cond);
-        spmm_rwr_tile<<<s->plan->sm_count, 512, 0, st>>>(a);
-        base += s->plan->sm_count;
+        BatchArgs a = batch_args(s, B, B->tiles[i], parity, base, total, i + 1 == nu, cond);
+        spmm_rwr_tile<<<sms, 512, 0, st>>>(a);
+        base += sms;
         cudaError_t e = cudaGetLastError();
         if (e) return e;
     }
@@ -256,11 +309,15 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         st = s->own_stream;
     }
     BatchState* B = static_cast<BatchState*>(s->batch);
-    spmv_plan_s* p = s->plan;
     if (!B) {
         B = new BatchState();
         s->batch = B;
         B->N = s->N;
+        spmv_status bs = build_batch_plan(s, B);
+        if (bs) return bs;
+    }
+    spmv_plan_s* p = B->plan;
+    if (!B->exec) {
         const size_t vec = (size_t)(s->N + 4) * kQP * sizeof(float);
 #define CKB(x) do { if ((e = (x)) != cudaSuccess) return cuda_status(e, #x); } while (0)
         CKB(cudaMalloc(&B->R, vec));
@@ -271,7 +328,7 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         if (p->num_tiles > 0) CKB(cudaMalloc(&B->Y, vec));
         CKB(cudaMalloc(&B->partials, (size_t)std::max<int64_t>(p->n_chunks, 1) * kQP * sizeof(float)));
         CKB(cudaMalloc(&B->q, kQP * sizeof(int32_t)));
-        const size_t nslots = (size_t)std::max<size_t>(s->tiles_used.size(), 1) * p->sm_count;
+        const size_t nslots = (size_t)std::max<size_t>(B->tiles.size(), 1) * p->sm_count;
         CKB(cudaMalloc(&B->slots, nslots * kQP * sizeof(double)));
         CKB(cudaMalloc(&B->res, kQP * sizeof(double)));
         // device-side loop: WHILE node around two iterations (double-buffered input)
@@ -354,6 +411,7 @@ void batch_destroy(spmv_solver s) {
     if (B->graph) cudaGraphDestroy(B->graph);
     cudaFree(B->R); cudaFree(B->Z[0]); cudaFree(B->Z[1]); cudaFree(B->Y); cudaFree(B->partials);
     cudaFree(B->q); cudaFree(B->slots); cudaFree(B->res);
+    if (B->plan) spmv_plan_destroy(B->plan);
     delete B;
     s->batch = nullptr;
 }

@@ -55,13 +55,16 @@ namespace tc {
 #define TC_DYN 2           // > 0: the last TC_DYN rounds of workloads are claimed dynamically; 0: static
 #endif
 #ifndef TC_PF_AHEAD
-#define TC_PF_AHEAD 2      // workloads of each warp bulk-prefetched into L2 ahead of use
+#define TC_PF_AHEAD 0      // L2 bulk prefetch of a warp's workload: 0 = when it starts, k > 0 =
+                           // k workloads ahead, -1 = none.  Measured on c2 (profiles/README.md):
+                           // 2 ahead keeps ~77 MB of future slots in L2 and evicts x (955 MB of
+                           // DRAM reads per SpMV); at start: 635 MB (algorithmic: 610 MB), -8 % time
 #endif
 #ifndef TC_PF_POLICY
 #define TC_PF_POLICY 0     // 1: prefetched slot lines enter L2 evict-first
 #endif
 #ifndef TC_X_POLICY
-#define TC_X_POLICY 0      // 1: x gathers carry an L2 evict-last policy (x stays resident)
+#define TC_X_POLICY 1      // 1: x gathers carry an L2 evict-last policy (x stays resident); -3 %
 #endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
@@ -415,9 +418,9 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
     // launch on the stream.
     const int64_t n_wl = a.wl_end - a.wl_begin;
     const int64_t rounds = n_wl / G;
-    // launches of fewer than four rounds stay fully dealt (measured: claiming there loses the
-    // two-ahead L2 prefetch and costs more than the imbalance it removes)
-    const int64_t s_end = rounds >= 4 && rounds > TC_DYN ? (rounds - TC_DYN) * G : n_wl;
+    // launches of fewer than eight rounds stay fully dealt (measured on c3 youtube: claiming
+    // there costs more than the imbalance it removes)
+    const int64_t s_end = rounds >= 8 && rounds > TC_DYN ? (rounds - TC_DYN) * G : n_wl;
     // the dealt sequence gw, gw + G, ... runs through the first dynamic round (s_end + gw)
     const int64_t dealt_end = s_end + G < n_wl ? s_end + G : n_wl;
     if (lane == 0) {
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
     for (int64_t j = gw; j < s_end; j += G) {
         const WlDesc d = load_desc(a.desc + a.wl_begin + j);
         const int64_t jn = j + (int64_t)kPrefetchAhead * G;
-        if (lane == 0 && jn < dealt_end) prefetch_workload<VALUED>(a, a.wl_begin + jn);
+        if (kPrefetchAhead >= 0 && lane == 0 && jn < dealt_end) prefetch_workload<VALUED>(a, a.wl_begin + jn);
         run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
     }
     // dynamic rounds: the first workload is still dealt (no burst of claims at the boundary);
@@ -440,10 +443,11 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
     int64_t jc = s_end + gw;
     while (jc < n_wl) {
         const WlDesc d = load_desc(a.desc + a.wl_begin + jc);
+        if (kPrefetchAhead == 0 && lane == 0) prefetch_workload<VALUED>(a, a.wl_begin + jc);
         int64_t jf = 0;
         if (lane == 0) jf = s_end + G + q + (int64_t)kDynQ * atomicAdd(a.sched + q, 1u);   // used after the workload
         run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
-        if (lane == 0 && jf < n_wl) prefetch_workload<VALUED>(a, a.wl_begin + jf);   // its later batches hit L2
+        if (kPrefetchAhead > 0 && lane == 0 && jf < n_wl) prefetch_workload<VALUED>(a, a.wl_begin + jf);
         jc = __shfl_sync(0xffffffffu, jf, 0);
     }
     __syncthreads();
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         const WlDesc d = load_desc(a.desc + j);
         // keep kPrefetchAhead workloads of this warp in flight from HBM into L2
         const int64_t jn = j + (int64_t)kPrefetchAhead * G;
-        if (lane == 0 && jn < a.wl_end) prefetch_workload<VALUED>(a, jn);
+        if (kPrefetchAhead >= 0 && lane == 0 && jn < a.wl_end) prefetch_workload<VALUED>(a, jn);
         run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
     }
 #endif

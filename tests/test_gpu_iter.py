@@ -116,6 +116,25 @@ def test_rwr_batch_parity(opt, gpu):
         s.run(int(qs[0]))
 
 
+@pytest.mark.parametrize("tw,tiles", [(1024, 1), (512, 3)])
+def test_rwr_batch_tiled_parity(tw, tiles, gpu, monkeypatch):
+    """The batch's own tiling (hub tile(s) whose 128-byte Z rows stay in L2, then the
+    remainder; first-touch / accumulate rows across tiles) against the oracle."""
+    from paper_1103_2405_b200 import Solver
+    monkeypatch.setenv("TCSPMV_BATCH_TW", str(tw))
+    monkeypatch.setenv("TCSPMV_BATCH_TILES", str(tiles))
+    G = graphgen.make_graph("t_mid")
+    s = Solver("rwr", G.n, G.row_ptr, G.col, device=0)
+    deg = np.diff(G.row_ptr) + np.bincount(G.col, minlength=G.n)
+    rng = np.random.default_rng(graphgen.SEED_QUERY)
+    qs = rng.choice(np.nonzero(deg > 0)[0], size=25, replace=False)
+    info = s.run_batch(qs)
+    R = s.result_batch()
+    for i, q in enumerate(qs[:8]):
+        ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, int(q), fixed_iters=info["iterations"])
+        assert np.abs(R[i].astype(np.float64) - ref).sum() < L1_BAR, (q, info)
+
+
 def test_config0_c1_pagerank_and_spmv(gpu):
     """BASELINE configs[0]: R-MAT scale 16 (65,536 vertices, 1M edges), PageRank d = 0.85 to
     1e-6 L1 and fp32 SpMV, against the oracle at full size."""
