@@ -93,13 +93,30 @@ struct TileArgs {
 
 // Slot loads: SMEM = false streams from global memory with evict-first (ld.global.cs); SMEM = true
 // reads slots the bulk-copy ring already placed in shared memory.
+#ifndef TC_STREAM_NA
+#define TC_STREAM_NA 0     // 1: 128-bit slot loads bypass L1 (L1::no_allocate), leaving L1 to x
+#endif
 template <bool SMEM> __device__ __forceinline__ int4 ld_i4(const int32_t* p) {
     if (SMEM) return *reinterpret_cast<const int4*>(p);
+#if TC_STREAM_NA
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+#else
     return __ldcs(reinterpret_cast<const int4*>(p));
+#endif
 }
 template <bool SMEM> __device__ __forceinline__ float4 ld_f4(const float* p) {
     if (SMEM) return *reinterpret_cast<const float4*>(p);
+#if TC_STREAM_NA
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+#else
     return __ldcs(reinterpret_cast<const float4*>(p));
+#endif
 }
 template <bool SMEM> __device__ __forceinline__ int2 ld_i2(const int32_t* p) {
     if (SMEM) return *reinterpret_cast<const int2*>(p);
@@ -138,7 +155,9 @@ struct XSrc {
 #if TC_X_POLICY
         {
             float v;
-            asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
+            if (hot <= 0) asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
+            else if (c < hot) asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
+            else asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
             return v;
         }
 #endif
