@@ -39,9 +39,12 @@ def main():
     opt = json.loads(os.environ.get("OPT", '{"num_tiles": 0, "workload_size": 1024}'))
     lib = os.path.basename(os.environ.get("TCSPMV_LIB", "libtcspmv.so"))
     y0 = None
+    base_env = dict(os.environ)
     for env in json.loads(os.environ.get("ENVS", "[{}]")):
         for k in ("TCSPMV_PREFIX", "TCSPMV_L1_HOT", "TCSPMV_CARVEOUT"):
             os.environ.pop(k, None)
+            if k in base_env:
+                os.environ[k] = base_env[k]
         os.environ.update({k: str(v) for k, v in env.items()})
         p = Plan(n, n, rp, col, val, device=0, **opt)
         for _ in range(5):

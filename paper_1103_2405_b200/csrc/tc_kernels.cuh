@@ -66,6 +66,9 @@ namespace tc {
 #ifndef TC_X_POLICY
 #define TC_X_POLICY 1      // 1: x gathers carry an L2 evict-last policy (x stays resident); -3 %
 #endif
+#ifndef TC_PIPE
+#define TC_PIPE 0          // 1: software-pipelined batches (next batch's slot loads overlap this batch's gathers)
+#endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
 #endif
@@ -169,6 +172,10 @@ struct XSrc {
     }
 };
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // one vector of KV slots: load cols (+vals), gather x, return the partial dot product
 template <int KV, bool VALUED, bool SMEM>
 struct Unit;
@@ -259,26 +266,53 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
     uint32_t ent_open = PAD_ROW;
     int32_t eix_open = -1;
     typename Epi::Pre pre_open{};
-    for (int v0 = 0; v0 < V; v0 += UB) {
-        Unit<4, VALUED, SMEM> u[UB];
-        bool ok[UB];
-        uint32_t ent_s[UB];
-        int32_t eix_s[UB];
-        typename Epi::Pre pre_s[UB];
+    Unit<4, VALUED, SMEM> u[UB];
+    bool ok[UB];
+    uint32_t ent_s[UB];
+    int32_t eix_s[UB];
+    // issue the slot loads (and row entries) of the batch starting at virtual unit b0
+    auto issue = [&](int b0, Unit<4, VALUED, SMEM>* uu, bool* okk, uint32_t* en, int32_t* ei) {
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
-            const int v = v0 + j;
+            const int v = b0 + j;
             const int step = v / upl, q = sl + (v - step * upl) * lpr;
             const int r = step * rps + sub;
-            ok[j] = v < V && r < d.h && q < w4;
-            if (ok[j]) u[j].load(wc + r * d.w, VALUED ? wv + r * d.w : nullptr, 4 * q);
+            okk[j] = v < V && r < d.h && q < w4;
+            if (okk[j]) uu[j].load(wc + r * d.w, VALUED ? wv + r * d.w : nullptr, 4 * q);
             // a row's entry and its epilogue operands are fetched when the row starts, so their
             // latency overlaps the row's slot loads and gathers
-            eix_s[j] = d.row_base + r;
-            ent_s[j] = (v < V && v % upl == 0 && sl == 0 && r < d.h) ? __ldg(a.row_id + eix_s[j]) : PAD_ROW;
+            ei[j] = d.row_base + r;
+            en[j] = (v < V && v % upl == 0 && sl == 0 && r < d.h) ? __ldg(a.row_id + ei[j]) : PAD_ROW;
         }
+    };
+    issue(0, u, ok, ent_s, eix_s);
+    for (int v0 = 0; v0 < V; v0 += UB) {
+        typename Epi::Pre pre_s[UB];
         #pragma unroll
         for (int j = 0; j < UB; ++j) pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j], eix_s[j]);
+#if TC_PIPE == 2
+        // the next batch's slot lines are pulled into L1 (no registers held) while this batch gathers
+        if (!SMEM) {
+            #pragma unroll
+            for (int j = 0; j < UB; ++j) {
+                const int v = v0 + UB + j;
+                const int step = v / upl, q = sl + (v - step * upl) * lpr;
+                const int r = step * rps + sub;
+                if (v < V && r < d.h && q < w4) {
+                    prefetch_l1(wc + r * d.w + 4 * q);
+                    if (VALUED) prefetch_l1(wv + r * d.w + 4 * q);
+                }
+            }
+        }
+#endif
+#if TC_PIPE == 1
+        // software pipeline: the next batch's slot loads are in flight while this batch gathers
+        Unit<4, VALUED, SMEM> un[UB];
+        bool okn[UB];
+        uint32_t ent_n[UB];
+        int32_t eix_n[UB];
+        issue(v0 + UB, un, okn, ent_n, eix_n);
+#endif
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int v = v0 + j;
@@ -294,6 +328,12 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
                 acc = 0.0f;
             }
         }
+#if TC_PIPE == 1
+        #pragma unroll
+        for (int j = 0; j < UB; ++j) { u[j] = un[j]; ok[j] = okn[j]; ent_s[j] = ent_n[j]; eix_s[j] = eix_n[j]; }
+#else
+        issue(v0 + UB, u, ok, ent_s, eix_s);
+#endif
     }
 }
 
@@ -312,21 +352,41 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
     const int32_t* cb = wc + lane * KV;
     const float* vb = VALUED ? wv + lane * KV : nullptr;
     float acc = 0.0f;
-    for (int u0 = 0; u0 < total; u0 += UB) {
-        Unit<KV, VALUED, SMEM> u[UB];
-        uint32_t ent[UB];
+    Unit<KV, VALUED, SMEM> u[UB];
+    uint32_t ent[UB];
+    auto issue = [&](int b0, Unit<KV, VALUED, SMEM>* uu, uint32_t* en) {
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
-            const int uu = u0 + j;
-            ent[j] = PAD_ROW;
-            if (uu < total) {
-                u[j].load(cb, vb, uu * (32 * KV));
-                if ((uu + 1) % nk == 0) ent[j] = __ldg(rid + 32 * (uu / nk));
+            const int q = b0 + j;
+            en[j] = PAD_ROW;
+            if (q < total) {
+                uu[j].load(cb, vb, q * (32 * KV));
+                if ((q + 1) % nk == 0) en[j] = __ldg(rid + 32 * (q / nk));
             }
         }
+    };
+    issue(0, u, ent);
+    for (int u0 = 0; u0 < total; u0 += UB) {
         typename Epi::Pre pre[UB];
         #pragma unroll
         for (int j = 0; j < UB; ++j) pre[j] = epi.prefetch(ent[j], d.row_base + lane + 32 * ((u0 + j) / nk));
+#if TC_PIPE == 2
+        if (!SMEM) {
+            #pragma unroll
+            for (int j = 0; j < UB; ++j) {
+                const int q = u0 + UB + j;
+                if (q < total) {
+                    prefetch_l1(cb + q * (32 * KV));
+                    if (VALUED) prefetch_l1(vb + q * (32 * KV));
+                }
+            }
+        }
+#endif
+#if TC_PIPE == 1
+        Unit<KV, VALUED, SMEM> un[UB];
+        uint32_t entn[UB];
+        issue(u0 + UB, un, entn);
+#endif
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int uu = u0 + j;
@@ -337,6 +397,12 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
                 acc = 0.0f;
             }
         }
+#if TC_PIPE == 1
+        #pragma unroll
+        for (int j = 0; j < UB; ++j) { u[j] = un[j]; ent[j] = entn[j]; }
+#else
+        issue(u0 + UB, u, ent);
+#endif
     }
 }
 
