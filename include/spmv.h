@@ -141,6 +141,15 @@ spmv_status spmv_execute_host(spmv_plan plan, const float* x_host, float* y_host
 
 spmv_status spmv_plan_stats(spmv_plan plan, spmv_plan_stats_t* out);
 spmv_status spmv_plan_layout(spmv_plan plan, spmv_layout_view* out);
+/* Write the layout arrays (Format v1) to `path` for the bit-exact format oracle
+ * (oracle/format_ref.py).  File: 8-byte magic "TCSPMV1\0", then int64
+ * n_rows, n_cols, n_workloads, n_row_entries, n_slots, n_split, n_tiles_total, valued (0/1),
+ * then, little endian and back to back: perm i32[n_cols], tiles i64[n_tiles_total*4],
+ * desc_off i64[nw], desc_row_base/w/h/split_id/chunk i32[nw] each, desc_kind u8[nw],
+ * desc_kvec u8[nw], row_id u32[n_row_entries], slot_col i32[n_slots], slot_val f32[n_slots]
+ * (valued plans only), split i32[n_split*3].  Errors: EINVAL (null), ENOMEM (file not writable),
+ * ECUDA (layout download). */
+spmv_status spmv_plan_export(spmv_plan plan, const char* path);
 /* Decode the layout back to COO (original row / column ids), padding dropped; arrays of nnz. */
 spmv_status spmv_plan_to_coo(spmv_plan plan, int32_t* rows, int32_t* cols, float* vals);
 /* Number of kernel launches one spmv_execute issues (x permutation included). */

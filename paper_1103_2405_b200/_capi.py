@@ -72,6 +72,7 @@ SIGNATURES = {
     "spmv_plan_stats": (c_i32, [c_vp, ctypes.POINTER(PlanStats)]),
     "spmv_plan_layout": (c_i32, [c_vp, ctypes.POINTER(LayoutView)]),
     "spmv_plan_to_coo": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "spmv_plan_export": (c_i32, [c_vp, ctypes.c_char_p]),
     "spmv_plan_launches": (c_i32, [c_vp]),
     "spmv_iter_opts_default": (None, [ctypes.POINTER(IterOpts), ctypes.c_int]),
     "spmv_solver_create": (c_i32, [ctypes.c_int, c_i64, c_i64, c_vp, c_vp, ctypes.POINTER(IterOpts),

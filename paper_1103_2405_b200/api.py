@@ -156,6 +156,10 @@ class Plan:
             split=arr(v.split, 3 * v.n_split, np.int32).reshape(-1, 3),
         )
 
+    def export(self, path: str) -> None:
+        """spmv_plan_export: the layout arrays as one binary file (include/spmv.h)."""
+        check(C.lib().spmv_plan_export(self._h, str(path).encode()), "spmv_plan_export")
+
     def to_coo(self):
         r = np.zeros(max(self.nnz, 1), np.int32)
         c = np.zeros(max(self.nnz, 1), np.int32)

@@ -1,4 +1,5 @@
 // capi.cu -- C ABI: plan creation, upload, spmv_execute (include/spmv.h).
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -356,6 +357,32 @@ spmv_status spmv_plan_layout(spmv_plan p, spmv_layout_view* v) {
     v->row_id = L.row_id.data(); v->slot_col = L.slot_col.data();
     v->slot_val = p->pattern ? nullptr : L.slot_val.data();
     v->split = L.split.data();
+    return SPMV_OK;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_plan_export(spmv_plan p, const char* path) {
+    if (!p || !path) { set_error("null argument"); return SPMV_EINVAL; }
+    spmv_layout_view v;
+    spmv_status s = spmv_plan_layout(p, &v);
+    if (s) return s;
+    FILE* f = std::fopen(path, "wb");
+    if (!f) { set_error(std::string("cannot open ") + path); return SPMV_ENOMEM; }
+    bool ok = true;
+    auto put = [&](const void* a, size_t bytes) { if (bytes && ok) ok = std::fwrite(a, 1, bytes, f) == bytes; };
+    const char magic[8] = {'T', 'C', 'S', 'P', 'M', 'V', '1', 0};
+    const int64_t hdr[8] = {p->n_rows, v.n_cols, v.n_workloads, v.n_row_entries, v.n_slots, v.n_split,
+                            v.n_tiles_total, p->pattern ? 0 : 1};
+    const size_t nw = (size_t)v.n_workloads;
+    put(magic, 8); put(hdr, sizeof(hdr));
+    put(v.perm, 4 * (size_t)v.n_cols); put(v.tiles, 32 * (size_t)v.n_tiles_total);
+    put(v.desc_off, 8 * nw); put(v.desc_row_base, 4 * nw); put(v.desc_w, 4 * nw); put(v.desc_h, 4 * nw);
+    put(v.desc_split_id, 4 * nw); put(v.desc_chunk, 4 * nw); put(v.desc_kind, nw); put(v.desc_kvec, nw);
+    put(v.row_id, 4 * (size_t)v.n_row_entries); put(v.slot_col, 4 * (size_t)v.n_slots);
+    if (!p->pattern) put(v.slot_val, 4 * (size_t)v.n_slots);
+    put(v.split, 12 * (size_t)v.n_split);
+    if (std::fclose(f) != 0) ok = false;
+    if (!ok) { set_error(std::string("short write to ") + path); return SPMV_ENOMEM; }
     return SPMV_OK;
 }
 

@@ -161,3 +161,57 @@ def test_no_device_means_loud_error():
     from paper_1103_2405_b200 import Plan, SpmvError
     with pytest.raises(SpmvError, match="ECUDA"):
         Plan(2, 2, np.array([0, 1, 2]), np.array([1, 0], np.int32), None, device=0)
+
+
+def read_export(path):
+    """Parse the spmv_plan_export file format (include/spmv.h) without the product's code."""
+    b = open(path, "rb").read()
+    assert b[:8] == b"TCSPMV1\0"
+    hdr = np.frombuffer(b, np.int64, 8, 8)
+    nr, nc, nw, ne, ns, nsp, nt, valued = (int(v) for v in hdr)
+    pos = 72
+    out = dict(n_rows=nr)
+
+    def take(name, dt, count):
+        nonlocal pos
+        a = np.frombuffer(b, dt, count, pos)
+        pos += a.nbytes
+        out[name] = a
+
+    take("perm", np.int32, nc)
+    take("tiles", np.int64, 4 * nt)
+    take("off", np.int64, nw)
+    for k in ("row_base", "w", "h", "split_id", "chunk"):
+        take(k, np.int32, nw)
+    take("kind", np.uint8, nw)
+    take("kvec", np.uint8, nw)
+    take("row_id", np.uint32, ne)
+    take("slot_col", np.int32, ns)
+    if valued:
+        take("slot_val", np.float32, ns)
+    take("split", np.int32, 3 * nsp)
+    assert pos == len(b)
+    return out
+
+
+@pytest.mark.parametrize("valued", [True, False])
+def test_export_file_matches_format_oracle(tmp_path, valued):
+    """spmv_plan_export writes the layout byte-identical to oracle/format_ref."""
+    rp, col, val = graphgen.random_csr(300, 280, 4000, seed=5, kind="powerlaw")
+    if not valued:
+        val = None
+    ref, p = build_both(300, 280, rp, col, val, 64, 2, [64, 128, 256])
+    path = tmp_path / "plan.bin"
+    p.export(path)
+    E = read_export(path)
+    assert np.array_equal(E["perm"], ref.perm)
+    assert np.array_equal(E["tiles"].reshape(ref.tiles.shape), ref.tiles)
+    for k in ("off", "row_base", "w", "h", "kind", "kvec", "split_id", "chunk"):
+        assert np.array_equal(E[k], ref.desc[k]), k
+    assert np.array_equal(E["row_id"], ref.row_id)
+    assert np.array_equal(E["slot_col"], ref.slot_col)
+    if valued:
+        assert E["slot_val"].tobytes() == ref.slot_val.tobytes()
+    else:
+        assert "slot_val" not in E
+    assert np.array_equal(E["split"].reshape(-1, 3), ref.split.reshape(-1, 3))
