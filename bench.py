@@ -241,23 +241,24 @@ def main():
     except Exception:
         pass
 
-    # end to end through the public API with host buffers (H2D x, D2H y inside every step)
-    xh = torch.from_numpy(x).pin_memory()
-    yh = torch.empty(G.n, dtype=torch.float32).pin_memory()
-    e2e_steps = max(5, args.steps // 10)
-    for _ in range(2):
-        pkg._capi.check(pkg.lib().spmv_execute_host(plan._h, ctypes.c_void_p(xh.data_ptr()),
-                                                     ctypes.c_void_p(yh.data_ptr()),
-                                                     ctypes.c_void_p(stream.cuda_stream)), "e2e")
+    # end to end through the public API with host buffers: spmv_execute_host_batch copies every
+    # step's x in (pinned H2D) and its y out (D2H) inside the timed region, overlapping the copies
+    # of neighbouring steps with the product (two copy streams, double-buffered)
+    e2e_steps = min(max(5, args.steps // 10), 32)
+    xh = torch.from_numpy(x).unsqueeze(0).expand(e2e_steps, G.n).contiguous().pin_memory()
+    yh = torch.empty((e2e_steps, G.n), dtype=torch.float32).pin_memory()
+
+    def e2e_call(cnt):
+        pkg._capi.check(pkg.lib().spmv_execute_host_batch(plan._h, ctypes.c_void_p(xh.data_ptr()),
+                                                           ctypes.c_void_p(yh.data_ptr()), cnt,
+                                                           ctypes.c_void_p(stream.cuda_stream)), "e2e")
+    e2e_call(3)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(e2e_steps):
-        pkg._capi.check(pkg.lib().spmv_execute_host(plan._h, ctypes.c_void_p(xh.data_ptr()),
-                                                     ctypes.c_void_p(yh.data_ptr()),
-                                                     ctypes.c_void_p(stream.cuda_stream)), "e2e")
+    e2e_call(e2e_steps)
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1) / e2e_steps
@@ -300,6 +301,19 @@ def main():
         cpu = {"value": round(2.0 * G.m / dtc / 1e9, 3), "unit": "GFLOP/s",
                "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                "sample": f"full c2 SpMV repeated {reps_cpu}x over ~10 s (fp64 CSR, OpenMP over rows)"}
+        # the paper-comparable one-thread CPU CSR run (SURVEY.md 8(d) "Oracle timing" (2))
+        try:
+            gomp = ctypes.CDLL("libgomp.so.1")
+            gomp.omp_set_num_threads(1)
+            reps1, tc0 = 0, time.perf_counter()
+            while time.perf_counter() - tc0 < 5.0:
+                oracle.spmv(G.row_ptr, G.col, val, x)
+                reps1 += 1
+            cpu["one_thread"] = {"value": round(2.0 * G.m * reps1 / (time.perf_counter() - tc0) / 1e9, 3),
+                                 "unit": "GFLOP/s", "cores": 1,
+                                 "sample": f"full c2 SpMV repeated {reps1}x over ~5 s, one OpenMP thread"}
+        finally:
+            gomp.omp_set_num_threads(len(os.sched_getaffinity(0)))
 
     # row-partitioned PageRank over all ranks (Sec. 3.2): one NCCL allgather per iteration
     if world > 1 and not os.environ.get("TCSPMV_BENCH_NO_DIST"):

@@ -139,6 +139,16 @@ spmv_status spmv_execute_timed(spmv_plan plan, const float* x_dev, float* y_dev,
 /* Host -> device -> host convenience: copies x (host), executes, copies y back, synchronises. */
 spmv_status spmv_execute_host(spmv_plan plan, const float* x_host, float* y_host, void* stream);
 
+/* Pipelined host -> device -> host over `count` independent products: y_b = A x_b for
+ * b = 0 .. count-1, x_host row-major [count][n_cols], y_host row-major [count][n_rows] (both
+ * caller-owned; pinned memory lets the copies run asynchronously). Two plan-owned device buffer
+ * pairs and two plan-owned copy streams overlap the H2D copy of x_{b+1}, the product b on
+ * `stream` and the D2H copy of y_{b-1}; every product still copies its own x in and its own y
+ * out. Synchronises before returning. Same per-product operation as spmv_execute (PAPER.md
+ * L291). Errors: SPMV_EINVAL (null pointer, count < 0), SPMV_ECUDA. */
+spmv_status spmv_execute_host_batch(spmv_plan plan, const float* x_host, float* y_host,
+                                    int32_t count, void* stream);
+
 spmv_status spmv_plan_stats(spmv_plan plan, spmv_plan_stats_t* out);
 spmv_status spmv_plan_layout(spmv_plan plan, spmv_layout_view* out);
 /* Write the layout arrays (Format v1) to `path` for the bit-exact format oracle

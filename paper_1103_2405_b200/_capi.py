@@ -68,6 +68,7 @@ SIGNATURES = {
     "spmv_execute": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "spmv_execute_permuted": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "spmv_execute_host": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "spmv_execute_host_batch": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "spmv_execute_timed": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
     "spmv_plan_stats": (c_i32, [c_vp, ctypes.POINTER(PlanStats)]),
     "spmv_plan_layout": (c_i32, [c_vp, ctypes.POINTER(LayoutView)]),

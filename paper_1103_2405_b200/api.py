@@ -124,6 +124,23 @@ class Plan:
                                         _stream_handle(stream)), "spmv_execute_host")
         return y[: self.n_rows]
 
+    def execute_host_batch(self, X, Y=None, stream=None):
+        """Y[b] = A X[b] for host arrays X [count, n_cols] -> Y [count, n_rows] (numpy or pinned
+        torch CPU tensors); copies in and out overlap the products (spmv_execute_host_batch)."""
+        if Y is None:
+            Y = np.empty((X.shape[0], self.n_rows), dtype=np.float32)
+        count = int(X.shape[0])
+        assert tuple(Y.shape) == (count, self.n_rows) and tuple(X.shape) == (count, self.n_cols)
+        xp = X.data_ptr() if hasattr(X, "data_ptr") else X.ctypes.data
+        yp = Y.data_ptr() if hasattr(Y, "data_ptr") else Y.ctypes.data
+        if hasattr(X, "is_contiguous"):
+            assert X.is_contiguous() and Y.is_contiguous()
+        else:
+            assert X.flags.c_contiguous and Y.flags.c_contiguous and X.dtype == np.float32 and Y.dtype == np.float32
+        check(C.lib().spmv_execute_host_batch(self._h, ctypes.c_void_p(xp), ctypes.c_void_p(yp), count,
+                                              _stream_handle(stream)), "spmv_execute_host_batch")
+        return Y
+
     @property
     def launches(self) -> int:
         return int(C.lib().spmv_plan_launches(self._h))

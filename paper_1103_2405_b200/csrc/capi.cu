@@ -53,7 +53,10 @@ static void free_device(spmv_plan_s* p) {
     cudaSetDevice(p->device);
     cudaFree(p->d_desc); cudaFree(p->d_row_id); cudaFree(p->d_col); cudaFree(p->d_val);
     cudaFree(p->d_perm); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
-    cudaFree(p->d_counters); cudaFree(p->d_hx); cudaFree(p->d_sched);
+    cudaFree(p->d_counters); cudaFree(p->d_hx); cudaFree(p->d_sched); cudaFree(p->d_hxb);
+    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+    for (auto& ev : p->ev_pipe) if (ev) cudaEventDestroy(ev);
     cudaSetDevice(cur);
 }
 
@@ -267,6 +270,54 @@ spmv_status spmv_execute_host(spmv_plan p, const float* xh, float* yh, void* str
     if (!s) s = spmv_execute(p, dx, dy, stream);
     if (!s && (e = cudaMemcpyAsync(yh, dy, p->n_rows * 4, cudaMemcpyDeviceToHost, st))) s = cuda_status(e, "D2H");
     if (!s && (e = cudaStreamSynchronize(st))) s = cuda_status(e, "sync");
+    return s;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_execute_host_batch(spmv_plan p, const float* xh, float* yh, int32_t count, void* stream) {
+    if (!p || ((!xh || !yh) && count > 0) || count < 0) { set_error("null argument or count < 0"); return SPMV_EINVAL; }
+    if (p->device < 0) { set_error("host-only plan cannot execute"); return SPMV_EINVAL; }
+    if (count == 0) return SPMV_OK;
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nx = std::max<int64_t>(p->n_cols, 1), ny = std::max<int64_t>(p->n_rows, 1);
+    if (!p->d_hxb) {
+        if ((e = cudaMalloc(&p->d_hxb, 2 * (nx + ny) * 4))) return cuda_status(e, "cudaMalloc");
+        if ((e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking))) return cuda_status(e, "stream");
+        if ((e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking))) return cuda_status(e, "stream");
+        for (auto& ev : p->ev_pipe)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_status(e, "event");
+    }
+    cudaEvent_t* h2d_done = p->ev_pipe;       // x buffer k filled
+    cudaEvent_t* comp_done = p->ev_pipe + 2;  // product on buffer pair k finished (x free, y ready)
+    cudaEvent_t* d2h_done = p->ev_pipe + 4;   // y buffer k drained
+    // the copy streams start after whatever the caller queued on `stream`
+    if ((e = cudaEventRecord(p->ev_pipe[6], st))) return cuda_status(e, "event");
+    cudaStreamWaitEvent(p->s_h2d, p->ev_pipe[6], 0);
+    cudaStreamWaitEvent(p->s_d2h, p->ev_pipe[6], 0);
+    spmv_status s = SPMV_OK;
+    for (int32_t b = 0; b < count && !s; ++b) {
+        const int k = b & 1;
+        float* dx = p->d_hxb + k * (nx + ny);
+        float* dy = dx + nx;
+        if (b >= 2) cudaStreamWaitEvent(p->s_h2d, comp_done[k], 0);   // product b-2 done with dx
+        if ((e = cudaMemcpyAsync(dx, xh + (int64_t)b * p->n_cols, p->n_cols * 4, cudaMemcpyHostToDevice, p->s_h2d)))
+            { s = cuda_status(e, "H2D"); break; }
+        cudaEventRecord(h2d_done[k], p->s_h2d);
+        cudaStreamWaitEvent(st, h2d_done[k], 0);
+        if (b >= 2) cudaStreamWaitEvent(st, d2h_done[k], 0);            // y of product b-2 drained
+        if ((s = spmv_execute(p, dx, dy, stream))) break;
+        cudaEventRecord(comp_done[k], st);
+        cudaStreamWaitEvent(p->s_d2h, comp_done[k], 0);
+        if ((e = cudaMemcpyAsync(yh + (int64_t)b * p->n_rows, dy, p->n_rows * 4, cudaMemcpyDeviceToHost, p->s_d2h)))
+            { s = cuda_status(e, "D2H"); break; }
+        cudaEventRecord(d2h_done[k], p->s_d2h);
+    }
+    // `stream` completes only after the last copy out
+    cudaEventRecord(p->ev_pipe[7], p->s_d2h);
+    cudaStreamWaitEvent(st, p->ev_pipe[7], 0);
+    if ((e = cudaStreamSynchronize(st)) && !s) s = cuda_status(e, "sync");
     return s;
 }
 

@@ -109,6 +109,15 @@ def test_graph_auto_and_deterministic(gpu):
         check(a, rp, col, val, x)
         yh = p.execute_host(x)                       # host path through the C ABI
         assert yh.tobytes() == a.tobytes()
+        # pipelined batch: 5 different x (odd count: both buffer pairs, ragged last round)
+        X = np.stack([graphgen.uniform_f32(G.n, seed=30 + b) for b in range(5)])
+        Y = p.execute_host_batch(X)
+        for b in range(5):
+            xt = torch.from_numpy(X[b]).cuda()
+            p.execute(xt, y1)
+            torch.cuda.synchronize()
+            assert Y[b].tobytes() == y1.cpu().numpy().tobytes()
+        assert p.execute_host_batch(X[:0]).shape == (0, G.n)
 
 
 def test_full_size_c2_sampled_rows(gpu):
