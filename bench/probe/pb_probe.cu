@@ -12,7 +12,7 @@
 
 struct Chunk { int64_t e0; int32_t n, col0, run0, nrun; };            // 24 B
 struct Run { int32_t start, len; int64_t goff; };                      // 16 B
-struct Bin { int64_t roff; int32_t rlen, row0, nrows, slab0, nslab, pad; };
+struct Bin { int64_t roff; int32_t rlen, row0, nrows, slab0, nslab, nheavy; int64_t hoff; };
 struct Slab { int64_t poff; int32_t w, mode; };                        // mode 0: ELL, 1: warp per row
 
 __device__ __forceinline__ uint64_t pol_last() {
@@ -22,66 +22,162 @@ __device__ __forceinline__ void st_last(float* a, float v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
 }
 
+#ifndef PB_FLAT
+#define PB_FLAT 1
+#endif
+#ifndef PB_CMAX
+#define PB_CMAX 16384
+#endif
+#ifndef PB_ET
+#define PB_ET 512
+#endif
+#ifndef PB_RT
+#define PB_RT 512
+#endif
 template <bool VALUED>
-__global__ void __launch_bounds__(1024) pb_expand(const Chunk* __restrict__ chunks, const Run* __restrict__ runs,
-                                                 const uint32_t* __restrict__ cd, const float* __restrict__ val,
-                                                 const float* __restrict__ x, float* __restrict__ buf) {
+__global__ void __launch_bounds__(PB_ET, 2) pb_expand(const Chunk* __restrict__ chunks, const Run* __restrict__ runs,
+                                                      const uint32_t* __restrict__ cd, const float* __restrict__ val,
+                                                      const float* __restrict__ x, float* __restrict__ buf) {
     extern __shared__ float stage[];
     const Chunk c = chunks[blockIdx.x];
     const uint32_t* p = cd + c.e0;
     const float* v = VALUED ? val + c.e0 : nullptr;
     const float* xb = x + c.col0;
-    for (int i = threadIdx.x; i < c.n; i += 1024) {
-        const uint32_t w = __ldcs(p + i);
-        float xv = __ldg(xb + (w & 0xffff));
-        if (VALUED) xv *= __ldcs(v + i);
-        stage[w >> 16] = xv;
+#if PB_FLAT
+    int* rs = reinterpret_cast<int*>(stage + PB_CMAX);            // run starts of this chunk
+    for (int r = threadIdx.x; r < c.nrun; r += PB_ET) rs[r] = __ldg(&runs[c.run0 + r].start);
+#endif
+    constexpr int U = 8;
+    for (int i0 = threadIdx.x; i0 < c.n; i0 += PB_ET * U) {
+        uint32_t w[U];
+        float a[U], xv[U];
+        #pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int i = i0 + j * PB_ET;
+            w[j] = i < c.n ? __ldcs(p + i) : 0xffffffffu;
+            if (VALUED) a[j] = i < c.n ? __ldcs(v + i) : 0.0f;
+        }
+        #pragma unroll
+        for (int j = 0; j < U; ++j) xv[j] = w[j] != 0xffffffffu ? __ldg(xb + (w[j] & 0xffff)) : 0.0f;
+        #pragma unroll
+        for (int j = 0; j < U; ++j)
+            if (w[j] != 0xffffffffu) stage[w[j] >> 16] = VALUED ? a[j] * xv[j] : xv[j];
     }
     __syncthreads();
     const uint64_t pol = pol_last();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int r = warp; r < c.nrun; r += 32) {
-        const Run ru = runs[c.run0 + r];
-        for (int k = lane; k < ru.len; k += 32) st_last(buf + ru.goff + k, stage[ru.start + k], pol);
+    // flat flush: warp w stores stage positions [q0, q0 + 32) for q0 = 32w, 32w + PB_ET, ...; the
+    // runs (sorted by stage start) are found with one ballot-free step per 32 positions: lanes hold
+    // a window of 32 run descriptors; runs starting inside the step set bits of a mask (redux.or),
+    // and lane i's run is the window base + popc(mask & lanes <= i) - 1 (+ the run open at q0)
+#if PB_FLAT
+    const Run* rt = runs + c.run0;
+    const int L = ((c.n + PB_ET / 32 - 1) / (PB_ET / 32) + 31) & ~31;   // positions per warp (multiple of 32)
+    const int q_beg = warp * L, q_end = min(c.n, q_beg + L);
+    if (q_beg < q_end) {
+        int lo = 0, hi = c.nrun - 1;                               // run containing q_beg
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rs[mid] <= q_beg) lo = mid; else hi = mid - 1;
+        }
+        for (int q0 = q_beg; q0 < q_end; q0 += 32) {
+            Run my{0, 0, 0};
+            if (lo + lane < c.nrun) my = rt[lo + lane];
+            const int d = my.start - q0;                           // run lo + lane starts at offset d
+            const unsigned bit = (lane > 0 && lo + lane < c.nrun && d >= 0 && d < 32) ? (1u << d) : 0u;
+            const unsigned M = __reduce_or_sync(0xffffffffu, bit);
+            const int j = __popc(M & (0xffffffffu >> (31 - lane)));   // runs started in [q0, q0 + lane]
+            const int st0 = __shfl_sync(0xffffffffu, my.start, j);
+            const long long go = __shfl_sync(0xffffffffu, (long long)my.goff, j);
+            const int q = q0 + lane;
+            if (q < q_end) st_last(buf + go + (q - st0), stage[q], pol);
+            lo += __popc(M);
+        }
     }
+#else
+    // each warp takes 32 runs at a time: one descriptor per lane (a single load round trip),
+    // then the warp stores the runs one after another (stores do not wait)
+    for (int r0 = warp * 32; r0 < c.nrun; r0 += PB_ET) {
+        Run my{0, 0, 0};
+        if (r0 + lane < c.nrun) my = runs[c.run0 + r0 + lane];
+        const int cnt = min(32, c.nrun - r0);
+        for (int j = 0; j < cnt; ++j) {
+            const int st0 = __shfl_sync(0xffffffffu, my.start, j);
+            const int len = __shfl_sync(0xffffffffu, my.len, j);
+            const long long go = __shfl_sync(0xffffffffu, (long long)my.goff, j);
+            for (int k = lane; k < len; k += 32) st_last(buf + go + k, stage[st0 + k], pol);
+        }
+    }
+#endif
 }
 
-__global__ void __launch_bounds__(1024) pb_reduce(const Bin* __restrict__ bins, const Slab* __restrict__ slabs,
-                                                 const uint16_t* __restrict__ pos, const int32_t* __restrict__ rowlen,
-                                                 const float* __restrict__ buf, float* __restrict__ y) {
+__global__ void __launch_bounds__(PB_RT, 2) pb_reduce(const Bin* __restrict__ bins, const Slab* __restrict__ slabs,
+                                                  const uint16_t* __restrict__ pos, const int64_t* __restrict__ rcum,
+                                                  const float* __restrict__ buf, float* __restrict__ y) {
     extern __shared__ float reg[];
+    __shared__ float wsum[PB_RT / 32];
     const Bin b = bins[blockIdx.x];
     const float* src = buf + b.roff;
-    for (int i = threadIdx.x; i < b.rlen; i += 1024) reg[i] = __ldcs(src + i);
+    {   // regions start 16-byte aligned (builder); float4 loads, four in flight per thread
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(reg);
+        const int n4 = (b.rlen + 3) >> 2;
+        for (int i0 = threadIdx.x; i0 < n4; i0 += PB_RT * 4) {
+            float4 t[4];
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) if (i0 + j * PB_RT < n4) t[j] = __ldcs(s4 + i0 + j * PB_RT);
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) if (i0 + j * PB_RT < n4) d4[i0 + j * PB_RT] = t[j];
+        }
+    }
+    __syncthreads();
     if (threadIdx.x == 0) reg[b.rlen] = 0.0f;                 // padding position -> 0
     __syncthreads();
+    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int s = warp; s < b.nslab; s += 32) {
-        const Slab sl = slabs[b.slab0 + s];
-        const int r0 = s * 32;
-        if (sl.mode == 0) {
-            const uint16_t* pp = pos + sl.poff + lane;
-            float acc = 0.0f;
-            int k = 0;
-            for (; k + 4 <= sl.w; k += 4) {
-                const uint16_t q0 = __ldcs(pp + 32 * k), q1 = __ldcs(pp + 32 * (k + 1));
-                const uint16_t q2 = __ldcs(pp + 32 * (k + 2)), q3 = __ldcs(pp + 32 * (k + 3));
-                acc += reg[q0]; acc += reg[q1]; acc += reg[q2]; acc += reg[q3];
-            }
-            for (; k < sl.w; ++k) acc += reg[__ldcs(pp + 32 * k)];
-            if (r0 + lane < b.nrows) y[b.row0 + r0 + lane] = acc;
-        } else {
-            // up to 32 rows, each at its own length, row-major
-            const uint16_t* pp = pos + sl.poff;
-            for (int rr = 0; rr < 32 && r0 + rr < b.nrows; ++rr) {
-                const int len = rowlen[b.row0 + r0 + rr];
-                float acc = 0.0f;
-                for (int k = lane; k < len; k += 32) acc += reg[__ldcs(pp + k)];
-                pp += len;
-                for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (lane == 0) y[b.row0 + r0 + rr] = acc;
-            }
+    // heavy rows (a prefix of the bin: rows are length-sorted), positions row-major at hoff
+    const int64_t c0 = rcum[b.row0];
+    int r = 0;
+    for (; r < b.nheavy; ++r) {                                 // giant rows: the whole CTA, fixed tree
+        const int64_t o = rcum[b.row0 + r] - c0, len = rcum[b.row0 + r + 1] - rcum[b.row0 + r];
+        if (len < 4096) break;
+        const uint16_t* pp = pos + b.hoff + o;
+        float acc = 0.0f;
+        for (int64_t k = threadIdx.x; k < len; k += PB_RT) acc += reg[__ldcs(pp + k)];
+        for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
+        if (lane == 0) wsum[warp] = acc;
+        __syncthreads();
+        if (warp == 0) {
+            float v = lane < PB_RT / 32 ? wsum[lane] : 0.0f;
+            for (int q = 16; q >= 1; q >>= 1) v += __shfl_xor_sync(0xffffffffu, v, q);
+            if (lane == 0) y[b.row0 + r] = v;
         }
+        __syncthreads();
+    }
+    for (int rr = r + warp; rr < b.nheavy; rr += PB_RT / 32) {          // warp per row
+        const int64_t o = rcum[b.row0 + rr] - c0, len = rcum[b.row0 + rr + 1] - rcum[b.row0 + rr];
+        const uint16_t* pp = pos + b.hoff + o;
+        float acc = 0.0f;
+        for (int64_t k = lane; k < len; k += 32) acc += reg[__ldcs(pp + k)];
+        for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
+        if (lane == 0) y[b.row0 + rr] = acc;
+    }
+    // light rows: 32-row ELL slabs after the heavy prefix, thread per row
+    for (int s = warp; s < b.nslab; s += PB_RT / 32) {
+        const Slab sl = slabs[b.slab0 + s];
+        const int rl = b.nheavy + s * 32 + lane;
+        const uint16_t* pp = pos + sl.poff + lane;
+        float acc = 0.0f;
+        int k = 0;
+        for (; k + 8 <= sl.w; k += 8) {
+            uint16_t q[8];
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = __ldcs(pp + 32 * (k + j));
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) acc += reg[q[j]];
+        }
+        for (; k < sl.w; ++k) acc += reg[__ldcs(pp + 32 * k)];
+        if (rl < b.nrows) y[b.row0 + rl] = acc;
     }
 }
 
@@ -93,19 +189,19 @@ int pb_setup(int stage_bytes, int region_bytes) {
     return (int)e;
 }
 // one SpMV: for each group g: expand chunks [gc[g], gc[g+1]), reduce bins [gb[g], gb[g+1])
-int pb_run(int G, const int32_t* gc, const int32_t* gb, const void* chunks, const void* runs,
+int pb_run(int G, int phases, const int32_t* gc, const int32_t* gb, const void* chunks, const void* runs,
            const uint32_t* cd, const float* val, const float* x, float* buf, const void* bins,
-           const void* slabs, const uint16_t* pos, const int32_t* rowlen, float* y, int stage_bytes, int region_bytes,
+           const void* slabs, const uint16_t* pos, const int64_t* rcum, float* y, int stage_bytes, int region_bytes,
            void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     for (int g = 0; g < G; ++g) {
         const int nc = gc[g + 1] - gc[g], nb = gb[g + 1] - gb[g];
         const Chunk* ch = (const Chunk*)chunks + gc[g];
-        if (nc > 0) {
-            if (val) pb_expand<true><<<nc, 1024, stage_bytes, st>>>(ch, (const Run*)runs, cd, val, x, buf);
-            else pb_expand<false><<<nc, 1024, stage_bytes, st>>>(ch, (const Run*)runs, cd, val, x, buf);
+        if (nc > 0 && (phases & 1)) {
+            if (val) pb_expand<true><<<nc, PB_ET, stage_bytes, st>>>(ch, (const Run*)runs, cd, val, x, buf);
+            else pb_expand<false><<<nc, PB_ET, stage_bytes, st>>>(ch, (const Run*)runs, cd, val, x, buf);
         }
-        if (nb > 0) pb_reduce<<<nb, 1024, region_bytes, st>>>((const Bin*)bins + gb[g], (const Slab*)slabs, pos, rowlen, buf, y);
+        if (nb > 0 && (phases & 2)) pb_reduce<<<nb, PB_RT, region_bytes, st>>>((const Bin*)bins + gb[g], (const Slab*)slabs, pos, rcum, buf, y);
     }
     return (int)cudaGetLastError();
 }

@@ -19,7 +19,7 @@ import graphgen  # noqa: E402
 CHUNK_DT = np.dtype([("e0", "<i8"), ("n", "<i4"), ("col0", "<i4"), ("run0", "<i4"), ("nrun", "<i4")])
 RUN_DT = np.dtype([("start", "<i4"), ("len", "<i4"), ("goff", "<i8")])
 BIN_DT = np.dtype([("roff", "<i8"), ("rlen", "<i4"), ("row0", "<i4"), ("nrows", "<i4"), ("slab0", "<i4"),
-                   ("nslab", "<i4"), ("pad", "<i4")])
+                   ("nslab", "<i4"), ("nheavy", "<i4"), ("hoff", "<i8")])
 SLAB_DT = np.dtype([("poff", "<i8"), ("w", "<i4"), ("mode", "<i4")])
 
 
@@ -84,7 +84,13 @@ def build(rp, col, n, G=4, C=8192, RB=24576, RROWS=8192, WMAX=64):
     runs = np.zeros(len(rstart), RUN_DT)
     runs["start"] = dest[first]
     runs["len"] = rlen
-    runs["goff"] = gpos[first] - ge[g1[first]]
+    # regions start 16-byte aligned: padded buffer position of every entry
+    bs0 = np.searchsorted(b1[o3], np.arange(nb + 1))
+    rl = np.diff(bs0)
+    rs_pad = np.concatenate([[0], np.cumsum((rl + 3) // 4 * 4)])
+    gbase = rs_pad[np.searchsorted(group_of_bin, np.arange(G + 1))]        # group buffer bases
+    gpos = gpos - bs0[b1] + rs_pad[b1]
+    runs["goff"] = gpos[first] - gbase[g1[first]]
     run_ch = ch_of[first]
     chunks = np.zeros(nch, CHUNK_DT)
     chunks["e0"] = cs[:-1]
@@ -97,53 +103,57 @@ def build(rp, col, n, G=4, C=8192, RB=24576, RROWS=8192, WMAX=64):
     cd = (colrel | (dest << 16)).astype(np.uint32)
     gc = np.searchsorted(g1[cs[:-1]], np.arange(G + 1)).astype(np.int32)
     # bins / regions
-    bs = np.searchsorted(b1[o3], np.arange(nb + 1))                 # region bounds (global positions)
     bins = np.zeros(nb, BIN_DT)
-    bins["roff"] = bs[:-1] - ge[group_of_bin]
-    bins["rlen"] = np.diff(bs)
+    bins["roff"] = rs_pad[:-1] - gbase[group_of_bin]
+    bins["rlen"] = rl
     assert bins["rlen"].max(initial=0) < 65535
     bins["row0"] = b0[:-1]
     bins["nrows"] = bin_rows
-    nsl = (bin_rows + 31) // 32
+    heavy = nlen > WMAX
+    nh = np.zeros(nb, np.int64)
+    np.add.at(nh, bin_of_row[heavy], 1)
+    bins["nheavy"] = nh
+    nl = bin_rows - nh
+    nsl = (nl + 31) // 32
     bins["nslab"] = nsl
     bins["slab0"] = np.concatenate([[0], np.cumsum(nsl)[:-1]])
     gb = np.searchsorted(group_of_bin, np.arange(G + 1)).astype(np.int32)
-    # slabs: rows of a bin in 32-row slabs; width = longest row (rows are length-sorted)
+    # pos layout: per bin, its heavy rows row-major (offset cum[r] - cum[row0]) then its light slabs
+    hlen = cum[b0[:-1] + nh] - cum[b0[:-1]]
     S = int(nsl.sum())
     slab_bin = np.repeat(np.arange(nb, dtype=np.int64), nsl)
-    slab_row0 = b0[:-1][slab_bin] + 32 * (np.arange(S) - bins["slab0"][slab_bin])
-    w = nlen[slab_row0]
+    slab_row0 = (b0[:-1] + nh)[slab_bin] + 32 * (np.arange(S) - bins["slab0"][slab_bin])
+    w = nlen[slab_row0] if S else np.zeros(0, np.int64)
     slabs = np.zeros(S, SLAB_DT)
     slabs["w"] = w
-    slabs["mode"] = (w > WMAX).astype(np.int32)
-    # mode-1 (warp per row) slabs store each row at its own length, row-major
-    real = np.minimum(32, np.maximum(0, bins["nrows"][slab_bin] - 32 * (np.arange(S) - bins["slab0"][slab_bin])))
-    slab_len = np.zeros(S, np.int64)
-    rows_cum = np.concatenate([[0], np.cumsum(nlen)])
-    slab_len = np.where(slabs["mode"] == 1, rows_cum[slab_row0 + real] - rows_cum[slab_row0], 32 * w)
-    slabs["poff"] = np.concatenate([[0], np.cumsum(slab_len)[:-1]])
-    npos = int(slab_len.sum())
+    blk = hlen + np.bincount(slab_bin, weights=32 * w, minlength=nb).astype(np.int64)   # pos per bin
+    bstart = np.concatenate([[0], np.cumsum(blk)[:-1]])
+    bins["hoff"] = bstart
+    within = np.concatenate([[0], np.cumsum(32 * w)[:-1]]) - np.concatenate([[0], np.cumsum(32 * w)])[bins["slab0"][slab_bin]]
+    slabs["poff"] = (bstart + hlen)[slab_bin] + within
+    npos = int(blk.sum())
     # positions: row's partials ordered by region position
-    lp = gpos - bs[b1]                                              # o1 order
+    lp = gpos - rs_pad[b1]                                          # o1 order
     rr = rnew[o1]
     o4 = np.lexsort((lp, rr))
     rr4, lp4 = rr[o4], lp[o4]
     k = np.arange(m) - cum[rr4]
-    slab = bins["slab0"][bin_of_row[rr4]] + (rr4 - b0[bin_of_row[rr4]]) // 32
-    lane = (rr4 - b0[bin_of_row[rr4]]) % 32
-    ww = w[slab]
-    idx = np.where(slabs["mode"][slab] == 0, slabs["poff"][slab] + k * 32 + lane,
-                   cum[rr4] - cum[slab_row0[slab]] + slabs["poff"][slab] + k)
+    bi = bin_of_row[rr4]
+    is_h = heavy[rr4]
+    lr = rr4 - b0[bi] - nh[bi]                                      # light row index in the bin
+    slab = bins["slab0"][bi] + np.maximum(lr, 0) // 32
+    lane = np.maximum(lr, 0) % 32
+    idx = np.where(is_h, bstart[bi] + cum[rr4] - cum[b0[bi]] + k,
+                   slabs["poff"][np.minimum(slab, max(S - 1, 0))] + k * 32 + lane)
     pos = np.empty(npos, np.uint16)
-    # padding -> the bin's rlen (region sentinel, zero in shared memory)
-    pad_bin = np.repeat(slab_bin, slab_len)
-    pos[:] = bins["rlen"][pad_bin].astype(np.uint16)
+    pad_bin = np.repeat(np.arange(nb), blk)
+    pos[:] = bins["rlen"][pad_bin].astype(np.uint16)                # padding -> region sentinel (zero)
     pos[idx] = lp4.astype(np.uint16)
     perm_val = o1                                                   # val in phase-1 order = val[o1]
     info = dict(m=m, n=n, G=G, chunks=nch, runs=len(runs), bins=nb, slabs=S, npos=npos,
-                mean_run=round(m / max(len(runs), 1), 1), max_group_entries=int(np.diff(ge).max()),
+                mean_run=round(m / max(len(runs), 1), 1), max_group_entries=int(np.diff(gbase).max()),
                 build_s=round(time.time() - t0, 1))
-    return dict(cd=cd, perm_val=perm_val, nlen=nlen.astype(np.int32), chunks=chunks, runs=runs, gc=gc, gb=gb, bins=bins, slabs=slabs,
+    return dict(cd=cd, perm_val=perm_val, nlen=nlen.astype(np.int32), rcum=cum.astype(np.int64), chunks=chunks, runs=runs, gc=gc, gb=gb, bins=bins, slabs=slabs,
                 pos=pos, rperm=rperm, ge=ge, info=info)
 
 
@@ -166,19 +176,16 @@ def emulate(T, x, val_o1):
         for bi in range(T["gb"][g], T["gb"][g + 1]):
             b = T["bins"][bi]
             reg = np.concatenate([buf[b["roff"]:b["roff"] + b["rlen"]], [0.0]])
+            for r in range(b["nheavy"]):
+                o = b["hoff"] + T["rcum"][b["row0"] + r] - T["rcum"][b["row0"]]
+                ln = T["nlen"][b["row0"] + r]
+                y[b["row0"] + r] = reg[T["pos"][o:o + ln].astype(np.int64)].sum()
             for s in range(b["nslab"]):
                 sl = T["slabs"][b["slab0"] + s]
-                if sl["mode"] == 0:
-                    P = T["pos"][sl["poff"]:sl["poff"] + 32 * sl["w"]].astype(np.int64)
-                    acc = reg[P.reshape(sl["w"], 32).T].sum(axis=1)
-                else:
-                    acc, o = np.zeros(32), sl["poff"]
-                    for lane in range(min(32, b["nrows"] - 32 * s)):
-                        ln = T["nlen"][b["row0"] + 32 * s + lane]
-                        acc[lane] = reg[T["pos"][o:o + ln].astype(np.int64)].sum()
-                        o += ln
+                P = T["pos"][sl["poff"]:sl["poff"] + 32 * sl["w"]].astype(np.int64)
+                acc = reg[P.reshape(sl["w"], 32).T].sum(axis=1)
                 for lane in range(32):
-                    r = s * 32 + lane
+                    r = b["nheavy"] + s * 32 + lane
                     if r < b["nrows"]:
                         y[b["row0"] + r] = acc[lane]
     return y
@@ -209,10 +216,10 @@ def main():
         return
     import torch
     lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpb_probe.so"))
-    stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 16, 4 * (T["bins"]["rlen"].max() + 1)
+    stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 4 * int(T["chunks"]["nrun"].max()) + 16, 4 * (T["bins"]["rlen"].max() + 8)
     assert lib.pb_setup(stage_b, int(region_b)) == 0
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
-    d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "nlen")}
+    d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "rcum")}
     dv = torch.from_numpy(val_o1).cuda() if val_o1 is not None else None
     xt = torch.from_numpy(x).cuda()
     buf = torch.empty(T["info"]["max_group_entries"] + 16, device="cuda")
@@ -222,9 +229,9 @@ def main():
     vp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
     stream = torch.cuda.current_stream().cuda_stream
 
-    def run():
-        rc = lib.pb_run(G, gc, gb, vp(d["chunks"]), vp(d["runs"]), vp(d["cd"]), vp(dv), vp(xt), vp(buf),
-                        vp(d["bins"]), vp(d["slabs"]), vp(d["pos"]), vp(d["nlen"]), vp(yt), stage_b, int(region_b),
+    def run(phases=3):
+        rc = lib.pb_run(G, phases, gc, gb, vp(d["chunks"]), vp(d["runs"]), vp(d["cd"]), vp(dv), vp(xt), vp(buf),
+                        vp(d["bins"]), vp(d["slabs"]), vp(d["pos"]), vp(d["rcum"]), vp(yt), stage_b, int(region_b),
                         ctypes.c_void_p(stream))
         assert rc == 0, rc
     run()
@@ -246,8 +253,17 @@ def main():
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) * 1000 / 50)
     us = float(np.median(res))
+    ph = {}
+    for mask in (1, 2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            run(mask)
+        e1.record()
+        torch.cuda.synchronize()
+        ph["expand_us" if mask == 1 else "reduce_us"] = round(e0.elapsed_time(e1) * 1000 / 20, 1)
     m = T["info"]["m"]
-    print(json.dumps(dict(cfg=cfg, pattern=pattern, ok=ok, deterministic=det, us=round(us, 1),
+    print(json.dumps(dict(cfg=cfg, pattern=pattern, ok=ok, deterministic=det, us=round(us, 1), **ph,
                           gflops=round(2 * m / us / 1e3, 1),
                           alg_GBps=round(((4 if pattern else 8) * m + 12 * Gr.n) / us / 1e3, 1),
                           static_bytes_per_nnz=round((4 * m + (0 if pattern else 4 * m) + 2 * T["info"]["npos"]) / m, 2),
