@@ -174,6 +174,9 @@ typedef struct {
     int32_t max_iter;      /* default 1000 */
     int32_t hits_norm;     /* 1 = halves sum to 1 (paper, L440; default), 2 = unit L2 halves */
     int32_t fixed_iters;   /* > 0: run exactly this many iterations (parity at equal k) */
+    int32_t exchange;      /* multi-GPU only: 0 = one allgather of every non-empty column (default);
+                            * 1 = needed columns: each rank receives only the values its rows read,
+                            *     by grouped NCCL send/recv (spmv_needed_lists) */
 } spmv_iter_opts;
 void spmv_iter_opts_default(spmv_iter_opts* o, int algo);
 
@@ -240,6 +243,19 @@ spmv_status bitonic_partition(int64_t n_rows, const int64_t* row_len, int32_t P,
  * Errors as bitonic_partition. */
 spmv_status spmv_partition_plan(int64_t n_rows, const int64_t* row_len, int32_t P, int32_t* owner_out,
                                 int64_t* local_index_out, int64_t* slot_rows);
+
+/* Needed-columns exchange lists for the row partition `owner` (the paper's row
+ * partition, Sec. 3.2, exchanging only what each partition reads, L106-L108).  M is the
+ * n x n iteration matrix (CSR: row i reads the columns col[row_ptr[i] .. row_ptr[i+1])).  For rank
+ * `rank`: send_count[q] = number of vertices owned by `rank` that rows owned by q read, recv_count[q]
+ * = number of vertices owned by q that rows owned by `rank` read (both 0 for q = rank); send_ids /
+ * recv_ids (optional, sized by the sums) receive the lists concatenated in rank order, each list
+ * ascending by vertex id -- the order both ends of a message use.  Host only (no device needed).
+ * Errors: EINVAL (null pointer, P < 1, rank outside [0,P), column outside [0,n)), ERANGE (owner
+ * outside [0,P)), ENOMEM. */
+spmv_status spmv_needed_lists(int64_t n, const int64_t* row_ptr, const int32_t* col, const int32_t* owner,
+                              int32_t P, int32_t rank, int64_t* send_count, int64_t* recv_count,
+                              int32_t* send_ids, int32_t* recv_ids);
 
 /* Communicator over NCCL (loaded at run time).  nccl_unique_id: the 128-byte ncclUniqueId,
  * created by rank 0 with spmv_comm_unique_id() and broadcast by the caller (e.g. over a torch

@@ -51,7 +51,7 @@ class LayoutView(ctypes.Structure):
 
 class IterOpts(ctypes.Structure):
     _fields_ = [("c", c_f64), ("tol", c_f64), ("max_iter", c_i32), ("hits_norm", c_i32),
-                ("fixed_iters", c_i32)]
+                ("fixed_iters", c_i32), ("exchange", c_i32)]
 
 
 class IterResult(ctypes.Structure):
@@ -74,6 +74,7 @@ SIGNATURES = {
     "spmv_plan_layout": (c_i32, [c_vp, ctypes.POINTER(LayoutView)]),
     "spmv_plan_to_coo": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "spmv_plan_export": (c_i32, [c_vp, ctypes.c_char_p]),
+    "spmv_needed_lists": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "spmv_plan_launches": (c_i32, [c_vp]),
     "spmv_iter_opts_default": (None, [ctypes.POINTER(IterOpts), ctypes.c_int]),
     "spmv_solver_create": (c_i32, [ctypes.c_int, c_i64, c_i64, c_vp, c_vp, ctypes.POINTER(IterOpts),

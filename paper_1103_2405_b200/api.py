@@ -304,6 +304,26 @@ def partition_plan(row_len, P: int):
     return owner[: len(rl)], lidx[: len(rl)], int(S.value)
 
 
+def needed_lists(row_ptr, col, owner, P: int, rank: int):
+    """(send, recv): per peer q, the ascending vertex ids `rank` sends to / receives from q in the
+    needed-columns exchange of the iteration matrix (row_ptr, col) under `owner` (spmv_needed_lists)."""
+    rp = _np(row_ptr, np.int64)
+    cl = _np(col, np.int32)
+    ow = _np(owner, np.int32)
+    n = len(rp) - 1
+    sc = np.zeros(P, np.int64)
+    rc = np.zeros(P, np.int64)
+    check(C.lib().spmv_needed_lists(n, _ptr(rp), _ptr(cl), _ptr(ow), int(P), int(rank), sc.ctypes.data,
+                                    rc.ctypes.data, None, None), "spmv_needed_lists")
+    si = np.zeros(max(int(sc.sum()), 1), np.int32)
+    ri = np.zeros(max(int(rc.sum()), 1), np.int32)
+    check(C.lib().spmv_needed_lists(n, _ptr(rp), _ptr(cl), _ptr(ow), int(P), int(rank), sc.ctypes.data,
+                                    rc.ctypes.data, si.ctypes.data, ri.ctypes.data), "spmv_needed_lists")
+    so = np.concatenate([[0], np.cumsum(sc)])
+    ro = np.concatenate([[0], np.cumsum(rc)])
+    return ([si[so[q]:so[q + 1]] for q in range(P)], [ri[ro[q]:ro[q + 1]] for q in range(P)])
+
+
 class Comm:
     """NCCL communicator for the row-partitioned path (Sec. 3.2).  The 128-byte unique id is
     created on rank 0 and broadcast by the caller (e.g. over a torch process group)."""

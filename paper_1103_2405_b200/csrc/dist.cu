@@ -27,6 +27,10 @@ struct Nccl {
     int (*CommDestroy)(NcclComm) = nullptr;
     int (*AllGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t) = nullptr;
     int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*Send)(const void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*Recv)(void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(int) = nullptr;
     bool load() {
         if (h) return true;
@@ -42,7 +46,12 @@ struct Nccl {
         AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
         AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
         GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-        return GetUniqueId && CommInitRank && CommDestroy && AllGather && AllReduce;
+        Send = (decltype(Send))dlsym(h, "ncclSend");
+        Recv = (decltype(Recv))dlsym(h, "ncclRecv");
+        GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+        GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
+        return GetUniqueId && CommInitRank && CommDestroy && AllGather && AllReduce && Send && Recv &&
+               GroupStart && GroupEnd;
     }
 };
 Nccl g_nccl;
@@ -89,6 +98,71 @@ spmv_status spmv_partition_plan(int64_t n_rows, const int64_t* row_len, int32_t 
     std::vector<int64_t> cnt(P, 0);
     for (int64_t i = 0; i < n_rows; ++i) local_index[i] = cnt[owner[i]]++;
     *slot_rows = n_rows ? *std::max_element(cnt.begin(), cnt.end()) : 0;
+    return SPMV_OK;
+}
+
+// Needed-columns exchange lists: rank r sends to q the values of the vertices r
+// owns that q's rows read; it receives from q the values of q's vertices its own rows read.
+// Both lists ascending by vertex id, so sender and receiver agree on the order without talking.
+static void needed_lists_impl(int64_t n, const int64_t* rp, const int32_t* col, const int32_t* owner,
+                              int32_t P, int32_t rank, std::vector<std::vector<int32_t>>& send,
+                              std::vector<std::vector<int32_t>>& recv) {
+    send.assign(P, {});
+    recv.assign(P, {});
+    std::vector<int32_t> stamp(n, -1);
+    // rows grouped by owner (ascending id within a rank)
+    std::vector<int64_t> cnt(P + 1, 0);
+    for (int64_t i = 0; i < n; ++i) cnt[owner[i] + 1]++;
+    for (int32_t q = 0; q < P; ++q) cnt[q + 1] += cnt[q];
+    std::vector<int64_t> rows(n), fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < n; ++i) rows[fill[owner[i]]++] = i;
+    for (int32_t q = 0; q < P; ++q) {
+        if (q == rank) continue;
+        std::vector<int32_t>& out = send[q];
+        for (int64_t t = cnt[q]; t < cnt[q + 1]; ++t) {
+            const int64_t i = rows[t];
+            for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+                const int32_t v = col[k];
+                if (owner[v] == rank && stamp[v] != q) { stamp[v] = q; out.push_back(v); }
+            }
+        }
+        std::sort(out.begin(), out.end());
+    }
+    std::fill(stamp.begin(), stamp.end(), -1);
+    for (int64_t t = cnt[rank]; t < cnt[rank + 1]; ++t) {
+        const int64_t i = rows[t];
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const int32_t v = col[k];
+            if (owner[v] != rank && stamp[v] != rank) { stamp[v] = rank; recv[owner[v]].push_back(v); }
+        }
+    }
+    for (auto& r : recv) std::sort(r.begin(), r.end());
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_needed_lists(int64_t n, const int64_t* row_ptr, const int32_t* col, const int32_t* owner,
+                              int32_t P, int32_t rank, int64_t* send_count, int64_t* recv_count,
+                              int32_t* send_ids, int32_t* recv_ids) {
+    if (n < 0 || (n > 0 && (!row_ptr || !owner)) || P < 1 || rank < 0 || rank >= P || !send_count || !recv_count) {
+        set_error("invalid argument"); return SPMV_EINVAL;
+    }
+    for (int64_t i = 0; i < n; ++i)
+        if (owner[i] < 0 || owner[i] >= P) { set_error("owner out of range"); return SPMV_ERANGE; }
+    if (n > 0 && row_ptr[n] > 0 && !col) { set_error("null col"); return SPMV_EINVAL; }
+    for (int64_t k = 0; k < (n > 0 ? row_ptr[n] : 0); ++k)
+        if (col[k] < 0 || col[k] >= n) { set_error("column out of range"); return SPMV_EINVAL; }
+    try {
+        std::vector<std::vector<int32_t>> send, recv;
+        needed_lists_impl(n, row_ptr, col, owner, P, rank, send, recv);
+        int64_t so = 0, ro = 0;
+        for (int32_t q = 0; q < P; ++q) {
+            send_count[q] = (int64_t)send[q].size();
+            recv_count[q] = (int64_t)recv[q].size();
+            if (send_ids) std::copy(send[q].begin(), send[q].end(), send_ids + so);
+            if (recv_ids) std::copy(recv[q].begin(), recv[q].end(), recv_ids + ro);
+            so += send_count[q]; ro += recv_count[q];
+        }
+    } catch (const std::bad_alloc&) { set_error("host allocation failed"); return SPMV_ENOMEM; }
     return SPMV_OK;
 }
 
@@ -143,9 +217,26 @@ struct Dist {
     std::vector<int32_t> owned;              // local row -> vertex
     std::vector<int64_t> lrow;               // vertex -> local row index on its owner
     int64_t q_local = -1;
-    float* d_G = nullptr;                    // gathered buffer: P slots
+    float* d_G = nullptr;                    // gathered buffer: P slots (needed mode: own slot + P-1 segments)
     int32_t* d_idx = nullptr;                // x'[k] = G[idx[k]] for k < nzc
+    int64_t* d_part_off = nullptr;           // [P] offset of rank q's fp64 partials in d_G
+    // needed-columns exchange (spmv_iter_opts.exchange = 1)
+    int exchange = 0;
+    std::vector<int64_t> soff, scnt, roff, rcnt;   // per peer: send / receive segment (floats, incl. partials)
+    float* d_S = nullptr;                    // send buffer
+    int32_t* d_sidx = nullptr;               // send position -> own slot position (-1: padding)
+    int64_t n_send = 0;
 };
+
+// send buffer: S[i] = own slot[sidx[i]] (values of the vertices a peer reads, then the partials)
+__global__ void dist_pack(const float* __restrict__ slot, const int32_t* __restrict__ sidx, float* __restrict__ S,
+                          int64_t n, const tc::Ctrl* ctrl) {
+    if (*(volatile const int32_t*)&ctrl->done) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = __ldg(sidx + i);
+        S[i] = j >= 0 ? slot[j] : 0.0f;
+    }
+}
 
 constexpr int64_t kPartialFloats = 8;        // four fp64 partials, 16-byte multiple
 
@@ -157,11 +248,11 @@ __global__ void dist_permute(const float* __restrict__ G, const int32_t* __restr
 }
 
 // sum the P ranks' partials in rank order (identical on every rank: deterministic), advance
-__global__ void dist_finalize(const float* G, int64_t slot, int64_t S, int P, tc::Ctrl* ctrl, int rwr) {
+__global__ void dist_finalize(const float* G, const int64_t* part_off, int P, tc::Ctrl* ctrl, int rwr) {
     if (threadIdx.x != 0 || *(volatile int32_t*)&ctrl->done) return;
     double res = 0.0, dm = 0.0;
     for (int r = 0; r < P; ++r) {
-        const double* part = reinterpret_cast<const double*>(G + (int64_t)r * slot + S);
+        const double* part = reinterpret_cast<const double*>(G + part_off[r]);
         res += part[0];
         dm += part[1];
     }
@@ -192,11 +283,11 @@ __global__ void gather_rows(const float* p_e, const int32_t* fpos, float* slot, 
 // derives the same half norms (rank-order sums), normalises its own rows (post) and the gathered
 // x it reads (permute).  The L1 change of a normalisation travels with the next exchange, so the
 // stop decision lags one SpMV and the reported iterate is the one that converged (reading R14).
-__global__ void hits_dist_finalize(const float* G, int64_t slot, int64_t S, int P, tc::Ctrl* ctrl, int l2) {
+__global__ void hits_dist_finalize(const float* G, const int64_t* part_off, int P, tc::Ctrl* ctrl, int l2) {
     if (threadIdx.x != 0 || *(volatile int32_t*)&ctrl->done) return;
     double s0 = 0.0, s1 = 0.0, r = 0.0;
     for (int k = 0; k < P; ++k) {
-        const double* part = reinterpret_cast<const double*>(G + (int64_t)k * slot + S);
+        const double* part = reinterpret_cast<const double*>(G + part_off[k]);
         s0 += part[0]; s1 += part[1]; r += part[2];
     }
     if (ctrl->iter >= 1) {
@@ -255,6 +346,22 @@ spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
     if (c->world == 1) return SPMV_OK;
     return nccl_status(g_nccl.AllGather(G + (int64_t)c->rank * slot, G, (size_t)slot, ncclFloat32, c->comm, st),
                        "ncclAllGather");
+}
+
+// the per-iteration exchange: one in-place allgather of equal slots, or (needed mode) the packed
+// per-peer segments by grouped point-to-point sends / receives
+spmv_status exchange(spmv_comm c, Dist* D, const tc::Ctrl* ctrl, int sm_count, cudaStream_t st) {
+    if (!D->exchange) return allgather(c, D->d_G, D->slot, st);
+    if (c->world == 1) return SPMV_OK;
+    if (D->n_send) dist_pack<<<sm_count * 2, 256, 0, st>>>(D->d_G, D->d_sidx, D->d_S, D->n_send, ctrl);
+    spmv_status s = nccl_status(g_nccl.GroupStart(), "ncclGroupStart");
+    for (int q = 0; q < D->P && !s; ++q) {
+        if (q == D->rank) continue;
+        s = nccl_status(g_nccl.Send(D->d_S + D->soff[q], (size_t)D->scnt[q], ncclFloat32, q, c->comm, st), "ncclSend");
+        if (!s) s = nccl_status(g_nccl.Recv(D->d_G + D->roff[q], (size_t)D->rcnt[q], ncclFloat32, q, c->comm, st), "ncclRecv");
+    }
+    spmv_status e = nccl_status(g_nccl.GroupEnd(), "ncclGroupEnd");
+    return s ? s : e;
 }
 
 }  // namespace
@@ -330,9 +437,48 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         spmv_plan_s* p = s->plan;
         // the plan's columns are ordered by local length: the first nzc have entries
         std::vector<int32_t> idx(D->nzc);
-        for (int64_t k = 0; k < D->nzc; ++k) {
-            idx[k] = (int32_t)D->gpos[p->perm[k]];
-            if (idx[k] < 0) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
+        std::vector<int64_t> part_off(D->P);
+        int64_t g_floats = (int64_t)D->P * D->slot;
+        D->exchange = s->it.exchange == 1;
+        if (!D->exchange) {
+            for (int64_t k = 0; k < D->nzc; ++k) {
+                idx[k] = (int32_t)D->gpos[p->perm[k]];
+                if (idx[k] < 0) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
+            }
+            for (int32_t q = 0; q < D->P; ++q) part_off[q] = (int64_t)q * D->slot + D->S;
+        } else {
+            // needed columns: own slot first, then one segment per peer holding the
+            // values of its vertices our rows read (ascending id, padded to 4 floats) + its partials
+            std::vector<std::vector<int32_t>> send, recv;
+            needed_lists_impl(n, mrp.data(), mcol.data(), owner.data(), D->P, D->rank, send, recv);
+            D->soff.assign(D->P, 0); D->scnt.assign(D->P, 0); D->roff.assign(D->P, 0); D->rcnt.assign(D->P, 0);
+            int64_t ro = D->slot, so = 0;
+            std::vector<int32_t> sidx;
+            for (int32_t q = 0; q < D->P; ++q) {
+                if (q == D->rank) { part_off[q] = D->S; continue; }
+                const int64_t rp4 = ((int64_t)recv[q].size() + 3) / 4 * 4;
+                D->roff[q] = ro; D->rcnt[q] = rp4 + kPartialFloats; part_off[q] = ro + rp4; ro += D->rcnt[q];
+                const int64_t sp4 = ((int64_t)send[q].size() + 3) / 4 * 4;
+                D->soff[q] = so; D->scnt[q] = sp4 + kPartialFloats; so += D->scnt[q];
+                for (int32_t v : send[q]) sidx.push_back((int32_t)D->lrow[v]);
+                for (int64_t j = (int64_t)send[q].size(); j < sp4; ++j) sidx.push_back(-1);
+                for (int64_t j = 0; j < kPartialFloats; ++j) sidx.push_back((int32_t)(D->S + j));
+            }
+            g_floats = ro;
+            D->n_send = so;
+            for (int64_t k = 0; k < D->nzc; ++k) {
+                const int32_t v = p->perm[k], q = owner[v];
+                if (q == D->rank) { idx[k] = (int32_t)D->lrow[v]; continue; }
+                auto it = std::lower_bound(recv[q].begin(), recv[q].end(), v);
+                if (it == recv[q].end() || *it != v) { set_error("internal: referenced column not received"); throw SPMV_EINVAL; }
+                idx[k] = (int32_t)(D->roff[q] + (it - recv[q].begin()));
+            }
+            if (so) {
+                if ((e = cudaMalloc(&D->d_S, so * sizeof(float))) || (e = cudaMalloc(&D->d_sidx, so * sizeof(int32_t))) ||
+                    (e = cudaMemcpy(D->d_sidx, sidx.data(), so * sizeof(int32_t), cudaMemcpyHostToDevice))) {
+                    st = cuda_status(e, "needed-columns buffers"); throw st;
+                }
+            }
         }
         std::vector<float> inv(std::max<int64_t>(D->n_local, 1), 0.0f);
         int64_t n_dangling = 0;
@@ -343,8 +489,10 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         }
         s->n_dangling = n_dangling;
 #define CKD(x) do { if ((e = (x)) != cudaSuccess) { st = cuda_status(e, #x); throw st; } } while (0)
-        CKD(cudaMalloc(&D->d_G, (size_t)D->P * D->slot * sizeof(float)));
-        CKD(cudaMemset(D->d_G, 0, (size_t)D->P * D->slot * sizeof(float)));
+        CKD(cudaMalloc(&D->d_G, (size_t)g_floats * sizeof(float)));
+        CKD(cudaMemset(D->d_G, 0, (size_t)g_floats * sizeof(float)));
+        CKD(cudaMalloc(&D->d_part_off, D->P * sizeof(int64_t)));
+        CKD(cudaMemcpy(D->d_part_off, part_off.data(), D->P * sizeof(int64_t), cudaMemcpyHostToDevice));
         CKD(cudaMalloc(&D->d_idx, std::max<int64_t>(D->nzc, 1) * sizeof(int32_t)));
         if (D->nzc) CKD(cudaMemcpy(D->d_idx, idx.data(), D->nzc * sizeof(int32_t), cudaMemcpyHostToDevice));
         const int64_t nl = std::max<int64_t>(D->n_local, 1);
@@ -427,7 +575,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     c.tele = rwr ? 0.0 : c.c * ((double)s->n_dangling / n) / n + (1.0 - c.c) / n;
     c.uniform = s->it.hits_norm == 1 ? 1.0 / n : 1.0 / std::sqrt(n);
     if ((e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st))) return cuda_status(e, "ctrl");
-    float* zslot = D->d_G + (int64_t)D->rank * D->slot;
+    float* zslot = D->exchange ? D->d_G : D->d_G + (int64_t)D->rank * D->slot;
     const int g = p->sm_count * 4;
     spmv_status ss = SPMV_OK;
     if (hitsa) {   // a(0) = h(0) = 1/|V| (L440): own rows and every gathered column
@@ -437,7 +585,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     } else {
         dist_init<<<g, 256, 0, st>>>(s->d_p, zslot, s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
         init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
-        if ((ss = allgather(s->comm, D->d_G, D->slot, st))) return ss;
+        if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
         dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
     }
     cudaEvent_t e0, e1;
@@ -461,8 +609,8 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                         return cuda_status(e, "tile launch");
                 }
                 if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
-                if ((ss = allgather(s->comm, D->d_G, D->slot, st))) return ss;
-                hits_dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->slot, D->S, D->P, s->d_ctrl, s->it.hits_norm != 1);
+                if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
+                hits_dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->d_part_off, D->P, s->d_ctrl, s->it.hits_norm != 1);
                 hits_dist_post<<<g, 512, 0, st>>>(zslot, s->d_p, D->d_half_local, D->n_local, s->d_ctrl, s->d_slots,
                                                   reinterpret_cast<double*>(zslot + D->S) + 2);
                 hits_dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, D->d_col_half, p->d_xp, D->nzc, s->d_ctrl);
@@ -481,8 +629,8 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                     return cuda_status(e, "tile launch");
             }
             if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
-            if ((ss = allgather(s->comm, D->d_G, D->slot, st))) return ss;
-            dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->slot, D->S, D->P, s->d_ctrl, rwr);
+            if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
+            dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->d_part_off, D->P, s->d_ctrl, rwr);
             dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
             ++launched;
         }
@@ -537,7 +685,11 @@ spmv_status solver_result_dist(spmv_solver s, float* out0, float* out1) {
 void solver_destroy_dist(spmv_solver s) {
     Dist* D = static_cast<Dist*>(s->dist);
     cudaSetDevice(s->device);
-    if (D) { cudaFree(D->d_G); cudaFree(D->d_idx); cudaFree(D->d_half_local); cudaFree(D->d_col_half); delete D; }
+    if (D) {
+        cudaFree(D->d_G); cudaFree(D->d_idx); cudaFree(D->d_half_local); cudaFree(D->d_col_half);
+        cudaFree(D->d_part_off); cudaFree(D->d_S); cudaFree(D->d_sidx);
+        delete D;
+    }
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
     cudaFree(s->d_p); cudaFree(s->d_y); cudaFree(s->d_inv); cudaFree(s->d_ctrl); cudaFree(s->d_slots);
     cudaFree(s->d_p_e); cudaFree(s->d_inv_e); cudaFree(s->d_fpos);

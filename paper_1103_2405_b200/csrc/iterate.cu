@@ -190,7 +190,7 @@ extern "C" {
 __attribute__((visibility("default"))) void spmv_iter_opts_default(spmv_iter_opts* o, int algo) {
     if (!o) return;
     o->c = algo == SPMV_ALGO_RWR ? 0.9 : 0.85;
-    o->tol = 1e-6; o->max_iter = 1000; o->hits_norm = 1; o->fixed_iters = 0;
+    o->tol = 1e-6; o->max_iter = 1000; o->hits_norm = 1; o->fixed_iters = 0; o->exchange = 0;
 }
 
 __attribute__((visibility("default")))

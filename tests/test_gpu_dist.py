@@ -57,3 +57,24 @@ def test_dist_hits_world1(norm, gpu):
     # the same number of normalisations as the single-GPU solver
     s1 = Solver("hits", G.n, G.row_ptr, G.col, device=0, iter_kw=dict(hits_norm=norm))
     assert abs(s1.run()["iterations"] - info["iterations"]) <= 1
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "rwr", "hits"])
+def test_dist_needed_exchange_world1(algo, gpu):
+    """exchange = 1 (needed columns): own-slot indexing, the partial-offset table
+    and the rank-order finalize on one GPU; parity with the oracle at the same iteration count."""
+    from paper_1103_2405_b200 import Solver
+    G = graphgen.make_graph("t_small")
+    s = Solver(algo, G.n, G.row_ptr, G.col, device=0, comm=comm1(), iter_kw=dict(exchange=1))
+    q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][3])
+    info = s.run(q) if algo == "rwr" else s.run()
+    if algo == "pagerank":
+        ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
+        assert np.abs(s.result().astype(np.float64) - ref).sum() < 1e-6, info
+    elif algo == "rwr":
+        ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, q, fixed_iters=info["iterations"])
+        assert np.abs(s.result().astype(np.float64) - ref).sum() < 1e-6, info
+    else:
+        a, h = s.result()
+        ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=1, fixed_iters=info["iterations"])
+        assert np.abs(a - ra).sum() < 1e-6 and np.abs(h - rh).sum() < 1e-6, info

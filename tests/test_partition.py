@@ -160,3 +160,113 @@ def test_gloo_pagerank_skip_empty_columns(tmp_path):
     for r in range(world):
         p = np.load(tmp_path / f"p{r}.npy")
         assert np.abs(p - ref).sum() < 1e-12
+
+
+# ---------------------------------------------------------------- needed-columns exchange (f3)
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+def test_needed_lists_brute_force(P):
+    """spmv_needed_lists against a set computation: rank r sends to q exactly the vertices r owns
+    that q's rows read, ascending; what r sends to q is what q expects from r."""
+    from paper_1103_2405_b200 import needed_lists, partition_plan
+    rp, col, _ = graphgen.random_csr(600, 600, 5000, seed=P, kind="powerlaw", valued=False)
+    owner, _, _ = partition_plan(np.diff(rp), P)
+    rows = np.repeat(np.arange(600), np.diff(rp))
+    lists = [needed_lists(rp, col, owner, P, r) for r in range(P)]
+    for r in range(P):
+        send, recv = lists[r]
+        for q in range(P):
+            if q == r:
+                assert len(send[q]) == 0 and len(recv[q]) == 0
+                continue
+            want_send = np.unique(col[(owner[rows] == q) & (owner[col] == r)])
+            want_recv = np.unique(col[(owner[rows] == r) & (owner[col] == q)])
+            assert np.array_equal(send[q], want_send) and np.array_equal(recv[q], want_recv)
+            assert np.array_equal(send[q], lists[q][1][r])      # sender and receiver agree
+
+
+def test_needed_lists_errors():
+    from paper_1103_2405_b200 import SpmvError, needed_lists
+    rp = np.array([0, 1, 2], np.int64)
+    col = np.array([1, 0], np.int32)
+    with pytest.raises(SpmvError):
+        needed_lists(rp, col, np.array([0, 2], np.int32), 2, 0)     # owner out of range
+    with pytest.raises(SpmvError):
+        needed_lists(rp, col, np.array([0, 1], np.int32), 2, 2)     # rank out of range
+    with pytest.raises(SpmvError):
+        needed_lists(rp, np.array([1, 5], np.int32), np.array([0, 1], np.int32), 2, 0)
+
+
+def _worker_pagerank_needed(rank, world, port, result_dir, iters):
+    """The needed-columns protocol of csrc/dist.cu (exchange = 1) in fp64 over gloo point-to-point:
+    each rank sends each peer the z values of the vertices on spmv_needed_lists' send list plus
+    its two fp64 partials, and builds its x from its own z and the received segments."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1103_2405_b200 import needed_lists, partition_plan
+    G = graphgen.make_graph("t_small")
+    n, c = G.n, 0.85
+    outdeg = np.diff(G.row_ptr)
+    rp, col = graphgen.keys_to_csr(G.keys, n, transpose=True)       # M = A^T
+    owner, _, _ = partition_plan(np.diff(rp), world)
+    send, recv = needed_lists(rp, col, owner, world, rank)
+    mine = np.nonzero(owner == rank)[0]
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    sel = owner[rows] == rank
+    inv_all = np.where(outdeg > 0, 1.0 / np.maximum(outdeg, 1), 0.0)
+    p = np.zeros(n)
+    p[mine] = 1.0 / n
+
+    def exchange(p, partials):
+        z = np.zeros(n)
+        z[mine] = p[mine] * inv_all[mine]
+        reqs, bufs = [], {}
+        for q in range(world):
+            if q == rank:
+                continue
+            out = torch.from_numpy(np.concatenate([z[send[q]], partials]))
+            bufs[q] = torch.zeros(len(recv[q]) + 2, dtype=torch.float64)
+            reqs.append(dist.isend(out, q))
+            reqs.append(dist.irecv(bufs[q], q))
+        for rq in reqs:
+            rq.wait()
+        tot = np.zeros(2)
+        for q in range(world):                                       # rank order
+            if q == rank:
+                tot += partials
+            else:
+                b = bufs[q].numpy()
+                z[recv[q]] = b[:len(recv[q])]
+                tot += b[len(recv[q]):]
+        return z, tot
+
+    z, tot = exchange(p, np.array([0.0, float(p[mine][outdeg[mine] == 0].sum())]))
+    D = tot[1]
+    for _ in range(iters):
+        y = np.bincount(rows[sel], weights=z[col[sel]], minlength=n)[mine]
+        pn = c * (y + D / n) + (1 - c) / n
+        part = np.array([float(np.abs(pn - p[mine]).sum()), float(pn[outdeg[mine] == 0].sum())])
+        p[mine] = pn
+        z, tot = exchange(p, part)
+        D = tot[1]
+    parts = [None] * world
+    dist.all_gather_object(parts, (mine.tolist(), p[mine].tolist()))
+    full = np.zeros(n)
+    for rws, vals in parts:
+        full[rws] = vals
+    np.save(os.path.join(result_dir, f"p{rank}.npy"), full)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_pagerank_needed_exchange(world, tmp_path):
+    iters = 12
+    port = _free_port()
+    mp.spawn(_worker_pagerank_needed, args=(world, port, str(tmp_path), iters), nprocs=world, join=True)
+    G = graphgen.make_graph("t_small")
+    ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=iters)
+    for r in range(world):
+        p = np.load(tmp_path / f"p{r}.npy")
+        assert np.abs(p - ref).sum() < 1e-12
