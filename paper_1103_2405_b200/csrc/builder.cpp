@@ -255,6 +255,11 @@ spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L)
             }
         }
         ti.wl_end = (int64_t)L.desc.size();
+        // descriptors address row entries and split partials with int32 (WlDesc::row_base, split table)
+        if ((int64_t)L.row_id.size() > (int64_t)INT32_MAX || L.n_chunks > (int64_t)INT32_MAX) {
+            set_error("more than 2^31-1 row entries or split chunks: use fewer tiles or a larger workload size");
+            return SPMV_ERANGE;
+        }
         // fill slots (parallel over this tile's workloads); rows of RM/CM workloads are
         // consecutive in `rows`, recovered from row_id entries
         L.slot_col.resize(n_slots, sentinel);
