@@ -238,6 +238,9 @@ def main():
             tr = json.load(f).get(launch_names[dom].split("(")[0])
             if tr:
                 roofline["traffic"] = tr
+                # effective DRAM bytes per stored entry vs the minimum 8 + 12 n / m
+                roofline["dram_bytes_per_nnz"] = round(tr / G.m, 2)
+                roofline["min_bytes_per_nnz"] = round(8 + 12 * G.n / G.m, 2)
     except Exception:
         pass
 
@@ -280,6 +283,7 @@ def main():
             extras[f"{algo}_iters_per_s"] = round(1e3 * info["iterations"] / info["ms_total"], 1)
             extras[f"{algo}_iterations"] = info["iterations"]
             extras[f"{algo}_us_per_iter"] = round(info["us_per_iter"], 2)
+            extras[f"{algo}_predicted_us_per_iter"] = round(info["predicted_us_per_iter"], 1)
             if algo == "rwr":
                 # the paper's 25 random queries (L448), batched as one SpMM per iteration (f1)
                 deg = np.diff(G.row_ptr) + np.bincount(G.col, minlength=G.n)
