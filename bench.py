@@ -275,6 +275,32 @@ def main():
 
     extras, cpu = {}, None
     if rank == 0 and world == 1 and not args.no_extras:
+        # BASELINE configs[0] (R-MAT s16, ~1 M entries; L2-resident: launch/latency-bound, so
+        # reported in microseconds, not against the roofline): SpMV and PageRank to 1e-6
+        import graphgen
+        G1 = graphgen.make_graph("c1")
+        v1 = graphgen.edge_values(G1.keys, seed=graphgen.SEED_VAL, mode=1)
+        p1 = pkg.Plan(G1.n, G1.n, G1.row_ptr, G1.col, v1, device=local)
+        x1 = torch.from_numpy(graphgen.uniform_f32(G1.n, seed=graphgen.SEED_X)).cuda()
+        y1 = torch.empty(G1.n, device="cuda")
+        for _ in range(10):
+            p1.execute(x1, y1, stream=stream)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(200):
+            p1.execute(x1, y1, stream=stream)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        extras["c1_spmv_us"] = round(g0.elapsed_time(g1) * 1e3 / 200, 2)
+        extras["c1_spmv_gflops"] = round(2 * G1.m / (extras["c1_spmv_us"] * 1e3), 1)
+        p1.close()
+        s1 = pkg.Solver("pagerank", G1.n, G1.row_ptr, G1.col, device=local)
+        s1.run()
+        i1 = s1.run()
+        extras["c1_pagerank_iterations"] = i1["iterations"]
+        extras["c1_pagerank_us_per_iter"] = round(i1["us_per_iter"], 2)
+        extras["c1_pagerank_iters_per_s"] = round(1e6 / i1["us_per_iter"], 1)
+        s1.close()
         for algo in ("pagerank", "hits", "rwr"):
             s = pkg.Solver(algo, G.n, G.row_ptr, G.col, device=local)
             q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][0]) if algo == "rwr" else 0

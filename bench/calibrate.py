@@ -48,11 +48,17 @@ def shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw):
     return n_rows, rp, col.astype(np.int32)
 
 
+N_DRAM = 64_000_000           # mode 3: x far beyond L2 (~50 M distinct columns referenced, ~200 MB)
+
+
 def measure(kind, w, h, mode, valued, target_slots, reps=5):
-    """mode 0: uncached, uniform columns; 1: cached (staged tile); 2: uncached, power-law columns"""
+    """mode 0: uncached, uniform columns; 1: cached (staged tile); 2: uncached, power-law columns;
+    3: uncached, uniform columns over an x that does not fit in L2 (gathers served by DRAM)"""
     cached = mode == 1
     rng = np.random.default_rng(w * 1000 + h)
-    n_cols = TW_CACHED if cached else N_UNCACHED
+    n_cols = TW_CACHED if cached else (N_DRAM if mode == 3 else N_UNCACHED)
+    if mode == 3:
+        target_slots = max(target_slots, 96_000_000)
     n_rows, rp, col = shape_matrix(kind, w, h, n_cols, target_slots, rng, powerlaw=mode == 2)
     val = rng.uniform(0, 1, len(col)).astype(np.float32) if valued else None
     opt = dict(tile_width=TW_CACHED if cached else n_cols, num_tiles=1 if cached else 0,
@@ -76,7 +82,41 @@ def measure(kind, w, h, mode, valued, target_slots, reps=5):
     return slots / (ms * 1e-3), ms, st["resident_warps"]
 
 
+def dram_regime():
+    """Mode 3 (x beyond L2, reading R32): entries = mode 0 x the measured mode-3 / mode-0 ratio of
+    its kind and value type, the ratio taken on representative shapes (a full mode-3 sweep needs a
+    96 M-entry matrix per shape).  Merged into the existing table."""
+    path = os.path.join(ROOT, "paper_1103_2405_b200", "data", "perf_table_b200.json")
+    with open(path) as f:
+        tab = json.load(f)
+    shapes = {"rm": [(128, 8), (1024, 1), (32, 32)], "cm": [(4, 256), (16, 64), (1, 1024)]}
+    ratio, detail = {}, []
+    for valued in (True, False):
+        for kind, lst in shapes.items():
+            r = []
+            for w, h in lst:
+                s0, _, _ = measure(kind, w, h, 0, valued, 96_000_000)
+                s3, _, _ = measure(kind, w, h, 3, valued, 96_000_000)
+                r.append(s3 / s0)
+                detail.append(dict(kind=kind, w=w, h=h, valued=valued, mode0=round(s0), mode3=round(s3)))
+                print(json.dumps(detail[-1]), flush=True)
+            ratio[(int(valued), KIND[kind])] = float(np.median(r))
+    entries = [e for e in tab["entries"] if e[0] != 3]
+    entries += [[3, e[1], e[2], e[3], e[4], round(e[5] * ratio[(e[1], e[2])], 1)] for e in tab["entries"] if e[0] == 0]
+    tab["entries"] = entries
+    tab["columns"][0] = "x mode (0 uncached uniform, 1 cached, 2 uncached power-law, 3 uncached beyond L2)"
+    tab["mode3_ratio"] = {f"valued={v},kind={k}": round(x, 4) for (v, k), x in ratio.items()}
+    tab["mode3_detail"] = detail
+    for p in (path, os.path.join(ROOT, "gpurun_out", "perf_table_b200.json")):
+        os.makedirs(os.path.dirname(p), exist_ok=True)
+        with open(p, "w") as f:
+            json.dump(tab, f, indent=0)
+    print(json.dumps(tab["mode3_ratio"]))
+
+
 def main():
+    if "--dram" in sys.argv:
+        return dram_regime()
     quick = "--quick" in sys.argv
     rm_w = [8, 32, 128, 512, 2048] if quick else [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
     rm_h = [1, 4, 16, 32] if quick else [1, 2, 4, 8, 16, 32]

@@ -45,6 +45,7 @@ struct PerfTable {
     double stage_GBps = 6000.0;     // chip-wide L2 -> shared memory staging bandwidth
     double rmw_GBps = 4000.0;       // y read-modify-write of accumulating rows
     double tail_frac = 0.0;         // launch tail: this fraction of one workload's duration under load
+    double l2_budget_bytes = 96e6;  // x spans above this are served by DRAM (mode 3, reading R32)
     int max_act_warp = 148 * 32;
     bool loaded = false;
     std::string source = "built-in";
@@ -54,7 +55,7 @@ struct PerfTable {
     // bilinear interpolation in (log2 w, log2 h), clamped to the measured range
     double lookup(int mode, bool valued, int kind, double w, double h) const {
         auto it = grids.find(key(mode, valued, kind));
-        if (it == grids.end() && mode == 2) it = grids.find(key(0, valued, kind));
+        if (it == grids.end() && (mode == 2 || mode == 3)) it = grids.find(key(0, valued, kind));
         const bool cached = mode == 1;
         if (it == grids.end() || it->second.lw.empty() || it->second.lh.empty()) return analytic(cached, valued, kind, w, h);
         const Grid& g = it->second;
@@ -107,6 +108,7 @@ static bool parse_table(const std::string& text, PerfTable& T) {
     if (num_after("rmw_GBps", v)) T.rmw_GBps = v;
     if (num_after("tail_frac", v)) T.tail_frac = v;
     if (num_after("max_act_warp", v)) T.max_act_warp = (int)v;
+    if (num_after("l2_budget_bytes", v)) T.l2_budget_bytes = v;
     size_t p = text.find("\"entries\"");
     if (p == std::string::npos) return false;
     p = text.find('[', p);
@@ -267,15 +269,26 @@ static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist,
 
 struct Choice { int32_t tw, T; std::vector<int32_t> wl; std::vector<double> us; double total; };
 
+// x regime of tile t (the offline table's x mode): 1 = staged in shared memory; otherwise 3 when
+// the tile's x span exceeds the L2 budget (gathers from DRAM, reading R32), 2 when the tile holds
+// the hub columns (single tile or unstaged first tile: hubs hit L1), else 0
+static int x_mode(const Prepared& P, int32_t tw, int32_t T, int32_t t, bool cached, const PerfTable& tab) {
+    if (cached) return 1;
+    const int64_t lo = std::min<int64_t>((int64_t)t * tw, P.n_cols);
+    const int64_t hi = t < T ? std::min<int64_t>((int64_t)(t + 1) * tw, P.n_cols) : P.n_cols;
+    if ((double)(hi - lo) * 4.0 > tab.l2_budget_bytes) return 3;
+    return t == 0 ? 2 : 0;
+}
+
 static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildParams& base, int32_t tw,
-                       int32_t T, const PerfTable& tab) {
+                       int32_t T, const PerfTable& tab, bool stage = true) {
     Choice c{tw, T, {}, {}, 0.0};
     std::vector<std::vector<std::pair<int64_t, int64_t>>> hist;
     tile_histograms(P, tw, T, hist);
     const bool valued = !P.pattern;
     for (int32_t t = 0; t <= T; ++t) {
-        const bool cached = t < T && opt.stage_x != 0;
-        const int mode = cached ? 1 : (T == 0 ? 2 : 0);
+        const bool cached = stage && t < T && opt.stage_x != 0;
+        const int mode = x_mode(P, tw, T, t, cached, tab);
         int32_t wl = kDefaultWL;
         double sec = 0.0;
         if (opt.workload_sizes) wl = opt.workload_sizes[std::min(t, opt.num_tiles >= 0 ? opt.num_tiles : t)];
@@ -333,6 +346,20 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
             if (c.total < best.total) best = c;
         }
         if (opt.num_tiles >= 0 && opt.tile_width > 0) break;
+    }
+    // x beyond L2 (c4-sized graphs): also L2-sized unstaged tiles, the paper's Solution 1 one
+    // level up (the tile's x segment stays in L2 instead of shared memory)
+    if (opt.tile_width <= 0 && (double)P.n_cols * 4.0 > tab.l2_budget_bytes) {
+        for (int32_t tw : {1 << 20, 1 << 21, 1 << 22, 1 << 23}) {
+            if ((double)tw * 4.0 > tab.l2_budget_bytes) continue;
+            const int64_t max_tiles = (P.n_cols + tw - 1) / tw;
+            for (int32_t T : {1, 2, 4}) {
+                if (opt.num_tiles >= 0 && T != opt.num_tiles) continue;
+                if (T >= max_tiles) continue;
+                Choice c = evaluate(P, opt, bp, tw, T, tab, false);
+                if (c.total < best.total) best = c;
+            }
+        }
     }
     if (best.wl.empty()) { set_error("no tiling candidate"); return SPMV_EINVAL; }
     bp.tile_width = best.tw;
