@@ -168,15 +168,25 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.time()
+        # the K timed steps in 5 batches with an event at each boundary (median and
+        # mean of 5 batches are reported beside the whole-run value; events do not sync)
+        nb = 5 if args.steps >= 5 else 1
+        bounds = [args.steps * i // nb for i in range(nb + 1)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(nb - 1)]
         e0.record(stream)
-        for _ in range(args.steps):
-            plan.execute(xt, yt)
+        for i in range(nb):
+            for _ in range(bounds[i + 1] - bounds[i]):
+                plan.execute(xt, yt)
+            if i < nb - 1:
+                ev[i].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
         t1 = time.time()
         if world > 1:
             dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    marks = [e0] + ev + [e1]
+    batch_ms = [marks[i].elapsed_time(marks[i + 1]) / max(bounds[i + 1] - bounds[i], 1) for i in range(nb)]
     if world > 1:
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -379,6 +389,8 @@ def main():
             "gpu_launches": int(args.steps * nl),
             "clocks": clk.summary(t0, t1),
             "predicted_us": round(st["predicted_us"], 2),
+            "batches_ms_per_step": {"n": nb, "median": round(float(np.median(batch_ms)), 5),
+                                    "mean": round(float(np.mean(batch_ms)), 5)},
         }
         line.update(extras)
         print(json.dumps(line), flush=True)

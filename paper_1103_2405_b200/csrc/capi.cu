@@ -29,6 +29,28 @@ __global__ void permute_x_kernel(const float* __restrict__ x, const int32_t* __r
     for (; i < n; i += stride) xp[i] = __ldg(x + __ldcs(perm + i));
 }
 
+// x'[inv[j]] = x[j]: x and inv read coalesced (16-byte vectors), x' written by scattered 4-byte
+// stores, which need no response (the gather form waits on 4.85 M random reads on c2)
+__global__ void scatter_x_kernel(const float* __restrict__ x, const int32_t* __restrict__ inv,
+                                 float* __restrict__ xp, int64_t n) {
+    const int64_t n4 = n >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int4* i4 = reinterpret_cast<const int4*>(inv);
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(inv)) & 15) == 0;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (vec) {
+        for (; i < n4; i += stride) {
+            const float4 v = __ldcs(x4 + i);
+            const int4 k = __ldcs(i4 + i);
+            xp[k.x] = v.x; xp[k.y] = v.y; xp[k.z] = v.z; xp[k.w] = v.w;
+        }
+        for (int64_t j = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) xp[inv[j]] = x[j];
+    } else {
+        for (; i < n; i += stride) xp[__ldcs(inv + i)] = __ldcs(x + i);
+    }
+}
+
 template <class T>
 static cudaError_t upload(T** dst, const std::vector<T>& src, int64_t& bytes) {
     size_t nb = std::max<size_t>(src.size(), 1) * sizeof(T);
@@ -46,13 +68,27 @@ static cudaError_t download(std::vector<T>& dst, const T* src, int64_t n) {
     return cudaMemcpy(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost);
 }
 
+static std::vector<int32_t> inverse(const std::vector<int32_t>& perm) {
+    std::vector<int32_t> inv(perm.size());
+    for (size_t k = 0; k < perm.size(); ++k) inv[perm[k]] = (int32_t)k;
+    return inv;
+}
+
+// x' = x relabelled (a7): scatter form by default, TCSPMV_PERMUTE=gather for the gather form
+static cudaError_t launch_permute(spmv_plan_s* p, const float* x, cudaStream_t st) {
+    int grid = (int)std::min<int64_t>((p->n_cols + 255) / 256, (int64_t)p->sm_count * 8);
+    if (p->permute_gather) permute_x_kernel<<<grid, 256, 0, st>>>(x, p->d_perm, p->d_xp, p->n_cols);
+    else scatter_x_kernel<<<grid, 256, 0, st>>>(x, p->d_inv, p->d_xp, p->n_cols);
+    return cudaGetLastError();
+}
+
 static void free_device(spmv_plan_s* p) {
     if (p->device < 0) return;
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
     cudaFree(p->d_desc); cudaFree(p->d_row_id); cudaFree(p->d_col); cudaFree(p->d_val);
-    cudaFree(p->d_perm); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
+    cudaFree(p->d_perm); cudaFree(p->d_inv); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
     cudaFree(p->d_counters); cudaFree(p->d_hx); cudaFree(p->d_sched); cudaFree(p->d_hxb);
     if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
     if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
@@ -121,6 +157,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
         int64_t& b = p->device_bytes;
         if ((e = upload(&p->d_desc, p->L.desc, b)) || (e = upload(&p->d_row_id, p->L.row_id, b)) ||
             (e = upload(&p->d_col, p->L.slot_col, b)) || (e = upload(&p->d_perm, p->perm, b)) ||
+            (e = upload(&p->d_inv, inverse(p->perm), b)) ||
             (e = upload(&p->d_split, p->L.split, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
@@ -136,6 +173,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
             (e = upload(&p->d_xp, xpz, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
+        if (const char* h = std::getenv("TCSPMV_PERMUTE")) p->permute_gather = std::string(h) == "gather";
         if (const char* h = std::getenv("TCSPMV_L1_HOT")) p->l1_hot_cols = std::atoi(h);
         if (const char* h = std::getenv("TCSPMV_PREFIX")) p->x_prefix = std::atoi(h) / 4 * 4;
         if (const char* h = std::getenv("TCSPMV_CARVEOUT")) p->l1_carveout = std::atoi(h);
@@ -246,9 +284,7 @@ spmv_status spmv_execute(spmv_plan p, const float* x, float* y, void* stream) {
     if (e) return cuda_status(e, "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
     if (p->n_cols > 0) {
-        int grid = (int)std::min<int64_t>((p->n_cols + 255) / 256, (int64_t)p->sm_count * 8);
-        permute_x_kernel<<<grid, 256, 0, st>>>(x, p->d_perm, p->d_xp, p->n_cols);
-        if ((e = cudaGetLastError())) return cuda_status(e, "permute_x");
+        if ((e = launch_permute(p, x, st))) return cuda_status(e, "permute_x");
     }
     return execute_permuted(p, p->d_xp, y, st);
 }
@@ -333,8 +369,7 @@ spmv_status spmv_execute_timed(spmv_plan p, const float* x, float* y, void* stre
     auto mark = [&]() { cudaEvent_t v; cudaEventCreate(&v); cudaEventRecord(v, st); ev.push_back(v); };
     mark();
     if (p->n_cols > 0) {
-        int grid = (int)std::min<int64_t>((p->n_cols + 255) / 256, (int64_t)p->sm_count * 8);
-        permute_x_kernel<<<grid, 256, 0, st>>>(x, p->d_perm, p->d_xp, p->n_cols);
+        launch_permute(p, x, st);
         mark();
     }
     for (int32_t t = 0; t <= p->num_tiles; ++t) {
