@@ -74,7 +74,8 @@ static std::vector<int32_t> inverse(const std::vector<int32_t>& perm) {
     return inv;
 }
 
-// x' = x relabelled (a7): scatter form by default, TCSPMV_PERMUTE=gather for the gather form
+// x' = x relabelled (a7): gather form by default; TCSPMV_PERMUTE=scatter selects the scatter form
+// (measured on c2: 354 vs 352 us per SpMV, profiles/r01_permute_forms.jsonl)
 static cudaError_t launch_permute(spmv_plan_s* p, const float* x, cudaStream_t st) {
     int grid = (int)std::min<int64_t>((p->n_cols + 255) / 256, (int64_t)p->sm_count * 8);
     if (p->permute_gather) permute_x_kernel<<<grid, 256, 0, st>>>(x, p->d_perm, p->d_xp, p->n_cols);
@@ -155,9 +156,10 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     if (device >= 0) {
         cudaError_t e;
         int64_t& b = p->device_bytes;
+        if (const char* h = std::getenv("TCSPMV_PERMUTE")) p->permute_gather = std::string(h) != "scatter";
         if ((e = upload(&p->d_desc, p->L.desc, b)) || (e = upload(&p->d_row_id, p->L.row_id, b)) ||
             (e = upload(&p->d_col, p->L.slot_col, b)) || (e = upload(&p->d_perm, p->perm, b)) ||
-            (e = upload(&p->d_inv, inverse(p->perm), b)) ||
+            (!p->permute_gather && (e = upload(&p->d_inv, inverse(p->perm), b))) ||
             (e = upload(&p->d_split, p->L.split, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
@@ -173,7 +175,6 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
             (e = upload(&p->d_xp, xpz, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
         }
-        if (const char* h = std::getenv("TCSPMV_PERMUTE")) p->permute_gather = std::string(h) == "gather";
         if (const char* h = std::getenv("TCSPMV_L1_HOT")) p->l1_hot_cols = std::atoi(h);
         if (const char* h = std::getenv("TCSPMV_PREFIX")) p->x_prefix = std::atoi(h) / 4 * 4;
         if (const char* h = std::getenv("TCSPMV_CARVEOUT")) p->l1_carveout = std::atoi(h);

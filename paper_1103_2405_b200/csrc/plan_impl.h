@@ -28,7 +28,7 @@ struct spmv_plan_s {
     float* d_val = nullptr;
     int32_t* d_perm = nullptr;
     int32_t* d_inv = nullptr;           // inverse relabel (scatter form of the x permutation)
-    bool permute_gather = false;        // TCSPMV_PERMUTE=gather: x'[k] = x[perm[k]] instead
+    bool permute_gather = true;         // x'[k] = x[perm[k]]; TCSPMV_PERMUTE=scatter: x'[inv[j]] = x[j]
     float* d_xp = nullptr;          // relabelled x for spmv_execute
     float* d_hx = nullptr;          // spmv_execute_host staging (x then y)
     float* d_hxb = nullptr;         // spmv_execute_host_batch: two (x, y) buffer pairs

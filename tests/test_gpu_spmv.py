@@ -169,15 +169,15 @@ def test_banded_matrices(half_band, drop, gpu):
 
 
 def test_permute_scatter_equals_gather(gpu, monkeypatch):
-    """a7: the scatter form x'[inv[j]] = x[j] (default) and the gather form x'[k] = x[perm[k]]
-    (TCSPMV_PERMUTE=gather) build the same x', so the products are bitwise equal; odd n_cols
+    """a7: the gather form x'[k] = x[perm[k]] (default) and the scatter form x'[inv[j]] = x[j]
+    (TCSPMV_PERMUTE=scatter) build the same x', so the products are bitwise equal; odd n_cols
     exercises the vector body and the scalar tail."""
     import torch
     from paper_1103_2405_b200 import Plan
     rp, col, val = graphgen.random_csr(3001, 4099, 60000, seed=5, kind="powerlaw", valued=True)
     x = torch.from_numpy(graphgen.uniform_f32(4099, seed=3)).cuda()
     out = []
-    for mode in (None, "gather"):
+    for mode in (None, "scatter"):
         if mode:
             monkeypatch.setenv("TCSPMV_PERMUTE", mode)
         p = Plan(3001, 4099, rp, col, val, device=0)
