@@ -155,3 +155,29 @@ def test_config0_c1_pagerank_and_spmv(gpu):
     y = plan.execute_host(x).astype(np.float64)
     yref, b = oracle.spmv(G.row_ptr, G.col, val, x)
     assert (np.abs(y - yref) <= 1e-5 * b + 1e-30).all()
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "hits", "rwr"])
+def test_config1_c2_full_size(algo, gpu):
+    """BASELINE configs[1] (LiveJournal-shaped, 4.85 M vertices, 69 M edges) at full size, with
+    the auto-tuned plan bench.py's extras use: the converged vector within 1e-6 L1 of the fp64
+    oracle run for the same iteration count (reading R14)."""
+    from paper_1103_2405_b200 import Solver
+    G = graphgen.make_graph("c2")
+    s = Solver(algo, G.n, G.row_ptr, G.col, device=0)
+    if algo == "rwr":
+        q = int(np.argmax(np.diff(G.row_ptr)))
+        info = s.run(q)
+        ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, q, fixed_iters=info["iterations"])
+        assert np.abs(s.result().astype(np.float64) - ref).sum() < L1_BAR, info
+    elif algo == "hits":
+        info = s.run()
+        a, h = s.result()
+        ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=1, fixed_iters=info["iterations"])
+        assert np.abs(a - ra).sum() < L1_BAR and np.abs(h - rh).sum() < L1_BAR, info
+    else:
+        info = s.run()
+        ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
+        assert np.abs(s.result().astype(np.float64) - ref).sum() < L1_BAR, info
+    assert info["converged"]
+    s.close()
