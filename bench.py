@@ -265,7 +265,7 @@ def main():
         pkg._capi.check(pkg.lib().spmv_execute_host_batch(plan._h, ctypes.c_void_p(xh.data_ptr()),
                                                            ctypes.c_void_p(yh.data_ptr()), cnt,
                                                            ctypes.c_void_p(stream.cuda_stream)), "e2e")
-    e2e_call(3)
+    e2e_call(e2e_steps)        # warm-up over every pinned page (first DMA to a page maps it)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

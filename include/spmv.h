@@ -141,7 +141,7 @@ spmv_status spmv_execute_host(spmv_plan plan, const float* x_host, float* y_host
 
 /* Pipelined host -> device -> host over `count` independent products: y_b = A x_b for
  * b = 0 .. count-1, x_host row-major [count][n_cols], y_host row-major [count][n_rows] (both
- * caller-owned; pinned memory lets the copies run asynchronously). Two plan-owned device buffer
+ * caller-owned; pinned memory lets the copies run asynchronously). Three plan-owned device buffer
  * pairs and two plan-owned copy streams overlap the H2D copy of x_{b+1}, the product b on
  * `stream` and the D2H copy of y_{b-1}; every product still copies its own x in and its own y
  * out. Synchronises before returning. Same per-product operation as spmv_execute (PAPER.md

@@ -320,30 +320,34 @@ spmv_status spmv_execute_host_batch(spmv_plan p, const float* xh, float* yh, int
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nx = std::max<int64_t>(p->n_cols, 1), ny = std::max<int64_t>(p->n_rows, 1);
     if (!p->d_hxb) {
-        if ((e = cudaMalloc(&p->d_hxb, 2 * (nx + ny) * 4))) return cuda_status(e, "cudaMalloc");
+        if ((e = cudaMalloc(&p->d_hxb, (int64_t)spmv_plan_s::kPipe * (nx + ny) * 4))) return cuda_status(e, "cudaMalloc");
         if ((e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking))) return cuda_status(e, "stream");
         if ((e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking))) return cuda_status(e, "stream");
         for (auto& ev : p->ev_pipe)
             if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_status(e, "event");
     }
     cudaEvent_t* h2d_done = p->ev_pipe;       // x buffer k filled
-    cudaEvent_t* comp_done = p->ev_pipe + 2;  // product on buffer pair k finished (x free, y ready)
-    cudaEvent_t* d2h_done = p->ev_pipe + 4;   // y buffer k drained
+    int NP = spmv_plan_s::kPipe;                   // buffer pairs in use (TCSPMV_PIPE = 2 or 3)
+    if (const char* v = std::getenv("TCSPMV_PIPE")) NP = std::max(2, std::min(spmv_plan_s::kPipe, std::atoi(v)));
+    constexpr int KP = spmv_plan_s::kPipe;
+    cudaEvent_t* comp_done = p->ev_pipe + KP;      // product on buffer pair k finished (x free, y ready)
+    cudaEvent_t* d2h_done = p->ev_pipe + 2 * KP;   // y buffer k drained
+    cudaEvent_t ev_start = p->ev_pipe[3 * KP], ev_end = p->ev_pipe[3 * KP + 1];
     // the copy streams start after whatever the caller queued on `stream`
-    if ((e = cudaEventRecord(p->ev_pipe[6], st))) return cuda_status(e, "event");
-    cudaStreamWaitEvent(p->s_h2d, p->ev_pipe[6], 0);
-    cudaStreamWaitEvent(p->s_d2h, p->ev_pipe[6], 0);
+    if ((e = cudaEventRecord(ev_start, st))) return cuda_status(e, "event");
+    cudaStreamWaitEvent(p->s_h2d, ev_start, 0);
+    cudaStreamWaitEvent(p->s_d2h, ev_start, 0);
     spmv_status s = SPMV_OK;
     for (int32_t b = 0; b < count && !s; ++b) {
-        const int k = b & 1;
+        const int k = b % NP;
         float* dx = p->d_hxb + k * (nx + ny);
         float* dy = dx + nx;
-        if (b >= 2) cudaStreamWaitEvent(p->s_h2d, comp_done[k], 0);   // product b-2 done with dx
+        if (b >= NP) cudaStreamWaitEvent(p->s_h2d, comp_done[k], 0);  // product b-NP done with dx
         if ((e = cudaMemcpyAsync(dx, xh + (int64_t)b * p->n_cols, p->n_cols * 4, cudaMemcpyHostToDevice, p->s_h2d)))
             { s = cuda_status(e, "H2D"); break; }
         cudaEventRecord(h2d_done[k], p->s_h2d);
         cudaStreamWaitEvent(st, h2d_done[k], 0);
-        if (b >= 2) cudaStreamWaitEvent(st, d2h_done[k], 0);            // y of product b-2 drained
+        if (b >= NP) cudaStreamWaitEvent(st, d2h_done[k], 0);           // y of product b-NP drained
         if ((s = spmv_execute(p, dx, dy, stream))) break;
         cudaEventRecord(comp_done[k], st);
         cudaStreamWaitEvent(p->s_d2h, comp_done[k], 0);
@@ -352,8 +356,8 @@ spmv_status spmv_execute_host_batch(spmv_plan p, const float* xh, float* yh, int
         cudaEventRecord(d2h_done[k], p->s_d2h);
     }
     // `stream` completes only after the last copy out
-    cudaEventRecord(p->ev_pipe[7], p->s_d2h);
-    cudaStreamWaitEvent(st, p->ev_pipe[7], 0);
+    cudaEventRecord(ev_end, p->s_d2h);
+    cudaStreamWaitEvent(st, ev_end, 0);
     if ((e = cudaStreamSynchronize(st)) && !s) s = cuda_status(e, "sync");
     return s;
 }

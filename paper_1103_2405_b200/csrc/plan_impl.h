@@ -31,9 +31,10 @@ struct spmv_plan_s {
     bool permute_gather = true;         // x'[k] = x[perm[k]]; TCSPMV_PERMUTE=scatter: x'[inv[j]] = x[j]
     float* d_xp = nullptr;          // relabelled x for spmv_execute
     float* d_hx = nullptr;          // spmv_execute_host staging (x then y)
-    float* d_hxb = nullptr;         // spmv_execute_host_batch: two (x, y) buffer pairs
+    float* d_hxb = nullptr;         // spmv_execute_host_batch: kPipe (x, y) buffer pairs
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // its copy streams
-    cudaEvent_t ev_pipe[8] = {};    // h2d done[2], compute done[2], d2h done[2]
+    static constexpr int kPipe = 3;
+    cudaEvent_t ev_pipe[3 * kPipe + 2] = {};   // h2d done[kPipe], compute done[kPipe], d2h done[kPipe], start, end
     int32_t* d_split = nullptr;
     float* d_partials = nullptr;
     int32_t* d_counters = nullptr;
