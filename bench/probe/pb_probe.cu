@@ -189,11 +189,41 @@ int pb_setup(int stage_bytes, int region_bytes) {
     return (int)e;
 }
 // one SpMV: for each group g: expand chunks [gc[g], gc[g+1]), reduce bins [gb[g], gb[g+1])
+// phases 4: expand of group g+1 (stream `stream`) overlaps the reduce of group g (a second
+// stream), with two group buffers at buf and buf + buf_stride
 int pb_run(int G, int phases, const int32_t* gc, const int32_t* gb, const void* chunks, const void* runs,
            const uint32_t* cd, const float* val, const float* x, float* buf, const void* bins,
            const void* slabs, const uint16_t* pos, const int64_t* rcum, float* y, int stage_bytes, int region_bytes,
-           void* stream) {
+           void* stream, long long buf_stride) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (phases == 4) {
+        static cudaStream_t s2 = nullptr;
+        static cudaEvent_t ex[64], rd[64], fin;
+        if (!s2) {
+            cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+            for (int i = 0; i < 64; ++i) { cudaEventCreateWithFlags(&ex[i], cudaEventDisableTiming); cudaEventCreateWithFlags(&rd[i], cudaEventDisableTiming); }
+            cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+        }
+        cudaEventRecord(fin, st);
+        cudaStreamWaitEvent(s2, fin, 0);
+        for (int g = 0; g < G; ++g) {
+            float* b = buf + (g & 1) * buf_stride;
+            const int nc = gc[g + 1] - gc[g], nb = gb[g + 1] - gb[g];
+            const Chunk* ch = (const Chunk*)chunks + gc[g];
+            if (g >= 2) cudaStreamWaitEvent(st, rd[g - 2], 0);        // buffer free again
+            if (nc > 0) {
+                if (val) pb_expand<true><<<nc, PB_ET, stage_bytes, st>>>(ch, (const Run*)runs, cd, val, x, b);
+                else pb_expand<false><<<nc, PB_ET, stage_bytes, st>>>(ch, (const Run*)runs, cd, val, x, b);
+            }
+            cudaEventRecord(ex[g], st);
+            cudaStreamWaitEvent(s2, ex[g], 0);
+            if (nb > 0) pb_reduce<<<nb, PB_RT, region_bytes, s2>>>((const Bin*)bins + gb[g], (const Slab*)slabs, pos, rcum, b, y);
+            cudaEventRecord(rd[g], s2);
+        }
+        cudaEventRecord(fin, s2);
+        cudaStreamWaitEvent(st, fin, 0);
+        return (int)cudaGetLastError();
+    }
     for (int g = 0; g < G; ++g) {
         const int nc = gc[g + 1] - gc[g], nb = gb[g + 1] - gb[g];
         const Chunk* ch = (const Chunk*)chunks + gc[g];

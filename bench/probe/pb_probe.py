@@ -222,17 +222,20 @@ def main():
     d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "rcum")}
     dv = torch.from_numpy(val_o1).cuda() if val_o1 is not None else None
     xt = torch.from_numpy(x).cuda()
-    buf = torch.empty(T["info"]["max_group_entries"] + 16, device="cuda")
+    stride = (T["info"]["max_group_entries"] + 16 + 63) // 64 * 64
+    buf = torch.empty(2 * stride, device="cuda")
+    overlap = os.environ.get("PB_OVERLAP", "0") == "1"
     yt = torch.full((Gr.n,), float("nan"), device="cuda")
     gc = (ctypes.c_int32 * len(T["gc"]))(*T["gc"].tolist())
     gb = (ctypes.c_int32 * len(T["gb"]))(*T["gb"].tolist())
     vp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
     stream = torch.cuda.current_stream().cuda_stream
 
-    def run(phases=3):
+    def run(phases=None):
+        phases = phases if phases is not None else (4 if overlap else 3)
         rc = lib.pb_run(G, phases, gc, gb, vp(d["chunks"]), vp(d["runs"]), vp(d["cd"]), vp(dv), vp(xt), vp(buf),
                         vp(d["bins"]), vp(d["slabs"]), vp(d["pos"]), vp(d["rcum"]), vp(yt), stage_b, int(region_b),
-                        ctypes.c_void_p(stream))
+                        ctypes.c_void_p(stream), ctypes.c_longlong(stride))
         assert rc == 0, rc
     run()
     torch.cuda.synchronize()
@@ -263,7 +266,7 @@ def main():
         torch.cuda.synchronize()
         ph["expand_us" if mask == 1 else "reduce_us"] = round(e0.elapsed_time(e1) * 1000 / 20, 1)
     m = T["info"]["m"]
-    print(json.dumps(dict(cfg=cfg, pattern=pattern, ok=ok, deterministic=det, us=round(us, 1), **ph,
+    print(json.dumps(dict(cfg=cfg, pattern=pattern, overlap=overlap, ok=ok, deterministic=det, us=round(us, 1), **ph,
                           gflops=round(2 * m / us / 1e3, 1),
                           alg_GBps=round(((4 if pattern else 8) * m + 12 * Gr.n) / us / 1e3, 1),
                           static_bytes_per_nnz=round((4 * m + (0 if pattern else 4 * m) + 2 * T["info"]["npos"]) / m, 2),
