@@ -12,7 +12,7 @@
 
 struct Chunk { int64_t e0; int32_t n, col0, run0, nrun; };            // 24 B
 struct Run { int32_t start, len; int64_t goff; };                      // 16 B
-struct Bin { int64_t roff; int32_t rlen, row0, nrows, slab0, nslab, nheavy; int64_t hoff; };
+struct Bin { int64_t roff; int32_t rlen, row0, nrows, slab0, nslab, nheavy; int64_t hoff; int32_t plen, pad2; };
 struct Slab { int64_t poff; int32_t w, mode; };                        // mode 0: ELL, 1: warp per row
 
 __device__ __forceinline__ uint64_t pol_last() {
@@ -24,6 +24,14 @@ __device__ __forceinline__ void st_last(float* a, float v, uint64_t pol) {
 
 #ifndef PB_FLAT
 #define PB_FLAT 1
+#endif
+#ifndef PB_POS_SMEM
+#define PB_POS_SMEM 0
+#endif
+#if PB_POS_SMEM
+#define LDP(p) (*(p))
+#else
+#define LDP(p) __ldcs(p)
 #endif
 #ifndef PB_CMAX
 #define PB_CMAX 16384
@@ -44,8 +52,14 @@ __global__ void __launch_bounds__(PB_ET, 2) pb_expand(const Chunk* __restrict__ 
     const float* v = VALUED ? val + c.e0 : nullptr;
     const float* xb = x + c.col0;
 #if PB_FLAT
-    int* rs = reinterpret_cast<int*>(stage + PB_CMAX);            // run starts of this chunk
-    for (int r = threadIdx.x; r < c.nrun; r += PB_ET) rs[r] = __ldg(&runs[c.run0 + r].start);
+    // run table of this chunk in shared memory: goff (8 B) then start (4 B) per run
+    long long* rg = reinterpret_cast<long long*>(stage + PB_CMAX);
+    int* rs = reinterpret_cast<int*>(rg + c.nrun);
+    for (int r = threadIdx.x; r < c.nrun; r += PB_ET) {
+        const Run ru = runs[c.run0 + r];
+        rs[r] = ru.start;
+        rg[r] = ru.goff;
+    }
 #endif
     constexpr int U = 8;
     for (int i0 = threadIdx.x; i0 < c.n; i0 += PB_ET * U) {
@@ -71,7 +85,6 @@ __global__ void __launch_bounds__(PB_ET, 2) pb_expand(const Chunk* __restrict__ 
     // a window of 32 run descriptors; runs starting inside the step set bits of a mask (redux.or),
     // and lane i's run is the window base + popc(mask & lanes <= i) - 1 (+ the run open at q0)
 #if PB_FLAT
-    const Run* rt = runs + c.run0;
     const int L = ((c.n + PB_ET / 32 - 1) / (PB_ET / 32) + 31) & ~31;   // positions per warp (multiple of 32)
     const int q_beg = warp * L, q_end = min(c.n, q_beg + L);
     if (q_beg < q_end) {
@@ -81,14 +94,14 @@ __global__ void __launch_bounds__(PB_ET, 2) pb_expand(const Chunk* __restrict__ 
             if (rs[mid] <= q_beg) lo = mid; else hi = mid - 1;
         }
         for (int q0 = q_beg; q0 < q_end; q0 += 32) {
-            Run my{0, 0, 0};
-            if (lo + lane < c.nrun) my = rt[lo + lane];
-            const int d = my.start - q0;                           // run lo + lane starts at offset d
-            const unsigned bit = (lane > 0 && lo + lane < c.nrun && d >= 0 && d < 32) ? (1u << d) : 0u;
+            const bool have = lo + lane < c.nrun;
+            const int mys = have ? rs[lo + lane] : 0x7fffffff;
+            const int d = mys - q0;                                // run lo + lane starts at offset d
+            const unsigned bit = (lane > 0 && have && d >= 0 && d < 32) ? (1u << d) : 0u;
             const unsigned M = __reduce_or_sync(0xffffffffu, bit);
             const int j = __popc(M & (0xffffffffu >> (31 - lane)));   // runs started in [q0, q0 + lane]
-            const int st0 = __shfl_sync(0xffffffffu, my.start, j);
-            const long long go = __shfl_sync(0xffffffffu, (long long)my.goff, j);
+            const int st0 = __shfl_sync(0xffffffffu, mys, j);
+            const long long go = rg[lo + j];
             const int q = q0 + lane;
             if (q < q_end) st_last(buf + go + (q - st0), stage[q], pol);
             lo += __popc(M);
@@ -130,6 +143,25 @@ __global__ void __launch_bounds__(PB_RT, 2) pb_reduce(const Bin* __restrict__ bi
             for (int j = 0; j < 4; ++j) if (i0 + j * PB_RT < n4) d4[i0 + j * PB_RT] = t[j];
         }
     }
+#if PB_POS_SMEM
+    // the bin's position block (heavy rows, then light slabs; 16-byte aligned, padded to 8) too
+    uint16_t* ps = reinterpret_cast<uint16_t*>(reg + ((b.rlen + 8 + 3) & ~3));
+    {
+        const uint4* s8 = reinterpret_cast<const uint4*>(pos + b.hoff);
+        uint4* d8 = reinterpret_cast<uint4*>(ps);
+        const int n8 = b.plen >> 3;
+        for (int i0 = threadIdx.x; i0 < n8; i0 += PB_RT * 4) {
+            uint4 t[4];
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) if (i0 + j * PB_RT < n8) t[j] = __ldcs(s8 + i0 + j * PB_RT);
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) if (i0 + j * PB_RT < n8) d8[i0 + j * PB_RT] = t[j];
+        }
+    }
+    const uint16_t* pbase = ps - b.hoff;                      // pbase[global pos index]
+#else
+    const uint16_t* pbase = pos;
+#endif
     __syncthreads();
     if (threadIdx.x == 0) reg[b.rlen] = 0.0f;                 // padding position -> 0
     __syncthreads();
@@ -141,9 +173,9 @@ __global__ void __launch_bounds__(PB_RT, 2) pb_reduce(const Bin* __restrict__ bi
     for (; r < b.nheavy; ++r) {                                 // giant rows: the whole CTA, fixed tree
         const int64_t o = rcum[b.row0 + r] - c0, len = rcum[b.row0 + r + 1] - rcum[b.row0 + r];
         if (len < 4096) break;
-        const uint16_t* pp = pos + b.hoff + o;
+        const uint16_t* pp = pbase + b.hoff + o;
         float acc = 0.0f;
-        for (int64_t k = threadIdx.x; k < len; k += PB_RT) acc += reg[__ldcs(pp + k)];
+        for (int64_t k = threadIdx.x; k < len; k += PB_RT) acc += reg[LDP(pp + k)];
         for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
         if (lane == 0) wsum[warp] = acc;
         __syncthreads();
@@ -156,9 +188,9 @@ __global__ void __launch_bounds__(PB_RT, 2) pb_reduce(const Bin* __restrict__ bi
     }
     for (int rr = r + warp; rr < b.nheavy; rr += PB_RT / 32) {          // warp per row
         const int64_t o = rcum[b.row0 + rr] - c0, len = rcum[b.row0 + rr + 1] - rcum[b.row0 + rr];
-        const uint16_t* pp = pos + b.hoff + o;
+        const uint16_t* pp = pbase + b.hoff + o;
         float acc = 0.0f;
-        for (int64_t k = lane; k < len; k += 32) acc += reg[__ldcs(pp + k)];
+        for (int64_t k = lane; k < len; k += 32) acc += reg[LDP(pp + k)];
         for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
         if (lane == 0) y[b.row0 + rr] = acc;
     }
@@ -166,17 +198,17 @@ __global__ void __launch_bounds__(PB_RT, 2) pb_reduce(const Bin* __restrict__ bi
     for (int s = warp; s < b.nslab; s += PB_RT / 32) {
         const Slab sl = slabs[b.slab0 + s];
         const int rl = b.nheavy + s * 32 + lane;
-        const uint16_t* pp = pos + sl.poff + lane;
+        const uint16_t* pp = pbase + sl.poff + lane;
         float acc = 0.0f;
         int k = 0;
         for (; k + 8 <= sl.w; k += 8) {
             uint16_t q[8];
             #pragma unroll
-            for (int j = 0; j < 8; ++j) q[j] = __ldcs(pp + 32 * (k + j));
+            for (int j = 0; j < 8; ++j) q[j] = LDP(pp + 32 * (k + j));
             #pragma unroll
             for (int j = 0; j < 8; ++j) acc += reg[q[j]];
         }
-        for (; k < sl.w; ++k) acc += reg[__ldcs(pp + 32 * k)];
+        for (; k < sl.w; ++k) acc += reg[LDP(pp + 32 * k)];
         if (rl < b.nrows) y[b.row0 + rl] = acc;
     }
 }

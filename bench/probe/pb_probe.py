@@ -19,7 +19,7 @@ import graphgen  # noqa: E402
 CHUNK_DT = np.dtype([("e0", "<i8"), ("n", "<i4"), ("col0", "<i4"), ("run0", "<i4"), ("nrun", "<i4")])
 RUN_DT = np.dtype([("start", "<i4"), ("len", "<i4"), ("goff", "<i8")])
 BIN_DT = np.dtype([("roff", "<i8"), ("rlen", "<i4"), ("row0", "<i4"), ("nrows", "<i4"), ("slab0", "<i4"),
-                   ("nslab", "<i4"), ("nheavy", "<i4"), ("hoff", "<i8")])
+                   ("nslab", "<i4"), ("nheavy", "<i4"), ("hoff", "<i8"), ("plen", "<i4"), ("pad2", "<i4")])
 SLAB_DT = np.dtype([("poff", "<i8"), ("w", "<i4"), ("mode", "<i4")])
 
 
@@ -127,8 +127,10 @@ def build(rp, col, n, G=4, C=8192, RB=24576, RROWS=8192, WMAX=64):
     slabs = np.zeros(S, SLAB_DT)
     slabs["w"] = w
     blk = hlen + np.bincount(slab_bin, weights=32 * w, minlength=nb).astype(np.int64)   # pos per bin
+    blk = (blk + 7) // 8 * 8                                         # 16-byte aligned blocks
     bstart = np.concatenate([[0], np.cumsum(blk)[:-1]])
     bins["hoff"] = bstart
+    bins["plen"] = blk
     within = np.concatenate([[0], np.cumsum(32 * w)[:-1]]) - np.concatenate([[0], np.cumsum(32 * w)])[bins["slab0"][slab_bin]]
     slabs["poff"] = (bstart + hlen)[slab_bin] + within
     npos = int(blk.sum())
@@ -216,7 +218,7 @@ def main():
         return
     import torch
     lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpb_probe.so"))
-    stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 4 * int(T["chunks"]["nrun"].max()) + 16, 4 * (T["bins"]["rlen"].max() + 8)
+    stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 12 * int(T["chunks"]["nrun"].max()) + 16, 4 * (T["bins"]["rlen"].max() + 12) + 2 * int(T["bins"]["plen"].max()) + 64
     assert lib.pb_setup(stage_b, int(region_b)) == 0
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
     d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "rcum")}
