@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tc_async.cuh"
+
 struct Chunk { int64_t e0; int32_t n, col0, run0, nrun; };            // 24 B
 struct Run { int32_t start, len; int64_t goff; };                      // 16 B
 struct Bin { int64_t roff; int32_t rlen, row0, nrows, slab0, nslab, nheavy; int64_t hoff; int32_t plen, pad2; };
@@ -213,11 +215,94 @@ __global__ void __launch_bounds__(PB_RT, 2) pb_reduce(const Bin* __restrict__ bi
     }
 }
 
+
+// persistent reduce: each CTA walks bins blockIdx.x, + gridDim.x, ...; the next bin's region is
+// bulk-copied (cp.async.bulk, TMA 1-D) into the other shared buffer while this one is summed
+__device__ __forceinline__ void reduce_bin(const Bin& b, const Slab* __restrict__ slabs,
+                                           const uint16_t* __restrict__ pos, const int64_t* __restrict__ rcum,
+                                           const float* reg, float* __restrict__ y, float* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c0 = rcum[b.row0];
+    int r = 0;
+    for (; r < b.nheavy; ++r) {
+        const int64_t o = rcum[b.row0 + r] - c0, len = rcum[b.row0 + r + 1] - rcum[b.row0 + r];
+        if (len < 4096) break;
+        const uint16_t* pp = pos + b.hoff + o;
+        float acc = 0.0f;
+        for (int64_t k = threadIdx.x; k < len; k += PB_RT) acc += reg[__ldcs(pp + k)];
+        for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
+        if (lane == 0) wsum[warp] = acc;
+        __syncthreads();
+        if (warp == 0) {
+            float v = lane < PB_RT / 32 ? wsum[lane] : 0.0f;
+            for (int q = 16; q >= 1; q >>= 1) v += __shfl_xor_sync(0xffffffffu, v, q);
+            if (lane == 0) y[b.row0 + r] = v;
+        }
+        __syncthreads();
+    }
+    for (int rr = r + warp; rr < b.nheavy; rr += PB_RT / 32) {
+        const int64_t o = rcum[b.row0 + rr] - c0, len = rcum[b.row0 + rr + 1] - rcum[b.row0 + rr];
+        const uint16_t* pp = pos + b.hoff + o;
+        float acc = 0.0f;
+        for (int64_t k = lane; k < len; k += 32) acc += reg[__ldcs(pp + k)];
+        for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
+        if (lane == 0) y[b.row0 + rr] = acc;
+    }
+    for (int s = warp; s < b.nslab; s += PB_RT / 32) {
+        const Slab sl = slabs[b.slab0 + s];
+        const int rl = b.nheavy + s * 32 + lane;
+        const uint16_t* pp = pos + sl.poff + lane;
+        float acc = 0.0f;
+        int k = 0;
+        for (; k + 8 <= sl.w; k += 8) {
+            uint16_t q[8];
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = __ldcs(pp + 32 * (k + j));
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) acc += reg[q[j]];
+        }
+        for (; k < sl.w; ++k) acc += reg[__ldcs(pp + 32 * k)];
+        if (rl < b.nrows) y[b.row0 + rl] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(PB_RT, 1) pb_reduce_pipe(const Bin* __restrict__ bins, int nbins, int buf_floats,
+                                                       const Slab* __restrict__ slabs, const uint16_t* __restrict__ pos,
+                                                       const int64_t* __restrict__ rcum, const float* __restrict__ buf,
+                                                       float* __restrict__ y) {
+    extern __shared__ __align__(128) float sm[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ float wsum[PB_RT / 32];
+    float* rb[2] = {sm, sm + buf_floats};
+    if (threadIdx.x == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); tc::fence_barrier_init(); }
+    __syncthreads();
+    const uint64_t pol = tc::policy_evict_first();
+    auto issue = [&](int j, int k) {
+        const Bin b = bins[j];
+        const uint32_t bytes = (uint32_t)(((b.rlen + 3) & ~3) * 4);
+        tc::mbar_arrive_expect_tx(&bar[k], bytes);
+        if (bytes) tc::bulk_g2s(rb[k], buf + b.roff, bytes, &bar[k], pol);
+    };
+    if (threadIdx.x == 0 && (int)blockIdx.x < nbins) issue(blockIdx.x, 0);
+    int i = 0;
+    for (int j = blockIdx.x; j < nbins; j += gridDim.x, ++i) {
+        const int cur = i & 1;
+        if (threadIdx.x == 0 && j + (int)gridDim.x < nbins) { tc::fence_proxy_async_shared(); issue(j + gridDim.x, cur ^ 1); }
+        const Bin b = bins[j];
+        tc::mbar_wait(&bar[cur], (i >> 1) & 1);
+        if (threadIdx.x == 0) rb[cur][b.rlen] = 0.0f;         // padding position -> 0
+        __syncthreads();
+        reduce_bin(b, slabs, pos, rcum, rb[cur], y, wsum);
+        __syncthreads();                                       // buffer free for the copy after next
+    }
+}
+
 extern "C" {
 int pb_setup(int stage_bytes, int region_bytes) {
     cudaError_t e = cudaFuncSetAttribute(pb_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
     if (!e) e = cudaFuncSetAttribute(pb_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
     if (!e) e = cudaFuncSetAttribute(pb_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, region_bytes);
+    if (!e) e = cudaFuncSetAttribute(pb_reduce_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * region_bytes + 256);
     return (int)e;
 }
 // one SpMV: for each group g: expand chunks [gc[g], gc[g+1]), reduce bins [gb[g], gb[g+1])
@@ -228,6 +313,8 @@ int pb_run(int G, int phases, const int32_t* gc, const int32_t* gb, const void* 
            const void* slabs, const uint16_t* pos, const int64_t* rcum, float* y, int stage_bytes, int region_bytes,
            void* stream, long long buf_stride) {
     cudaStream_t st = (cudaStream_t)stream;
+    const bool pipe_reduce = phases == 8;
+    if (phases == 8) phases = 4;
     if (phases == 4) {
         static cudaStream_t s2 = nullptr;
         static cudaEvent_t ex[64], rd[64], fin;
@@ -249,7 +336,17 @@ int pb_run(int G, int phases, const int32_t* gc, const int32_t* gb, const void* 
             }
             cudaEventRecord(ex[g], st);
             cudaStreamWaitEvent(s2, ex[g], 0);
-            if (nb > 0) pb_reduce<<<nb, PB_RT, region_bytes, s2>>>((const Bin*)bins + gb[g], (const Slab*)slabs, pos, rcum, b, y);
+            if (nb > 0) {
+                if (pipe_reduce) {
+                    static int sms = 0;
+                    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                    const int bf = ((region_bytes / 4) + 31) & ~31;
+                    pb_reduce_pipe<<<nb < sms ? nb : sms, PB_RT, 2 * bf * 4, s2>>>((const Bin*)bins + gb[g], nb, bf,
+                                                                                  (const Slab*)slabs, pos, rcum, b, y);
+                } else {
+                    pb_reduce<<<nb, PB_RT, region_bytes, s2>>>((const Bin*)bins + gb[g], (const Slab*)slabs, pos, rcum, b, y);
+                }
+            }
             cudaEventRecord(rd[g], s2);
         }
         cudaEventRecord(fin, s2);

@@ -218,7 +218,7 @@ def main():
         return
     import torch
     lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpb_probe.so"))
-    stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 12 * int(T["chunks"]["nrun"].max()) + 16, 4 * (T["bins"]["rlen"].max() + 12) + 2 * int(T["bins"]["plen"].max()) + 64
+    stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 12 * int(T["chunks"]["nrun"].max()) + 16, 4 * (T["bins"]["rlen"].max() + 12) + (2 * int(T["bins"]["plen"].max()) + 64 if os.environ.get("PB_POS_SMEM") == "1" else 0)
     assert lib.pb_setup(stage_b, int(region_b)) == 0
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
     d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "rcum")}
@@ -234,7 +234,7 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
 
     def run(phases=None):
-        phases = phases if phases is not None else (4 if overlap else 3)
+        phases = phases if phases is not None else ((8 if os.environ.get("PB_PIPE") == "1" else 4) if overlap else 3)
         rc = lib.pb_run(G, phases, gc, gb, vp(d["chunks"]), vp(d["runs"]), vp(d["cd"]), vp(dv), vp(xt), vp(buf),
                         vp(d["bins"]), vp(d["slabs"]), vp(d["pos"]), vp(d["rcum"]), vp(yt), stage_b, int(region_b),
                         ctypes.c_void_p(stream), ctypes.c_longlong(stride))
