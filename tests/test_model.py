@@ -131,3 +131,44 @@ def test_eq1_waves_in_product(tmp_path):
     # WL=1, rows of length 1: w=1 >= hq=1 -> row major, padded to 8 slots; 2000 workloads
     us = p.stats()["tile_predicted_us"][0]
     assert math.isclose(us, 2000 * 8 / 1e9 * 1e6 + TABLE["launch_us"], rel_tol=1e-12)
+
+
+# per x regime constants (mode: (rm, cm) slots/s): 0 uncached uniform, 1 staged, 2 hub tile, 3 beyond L2
+PERF_MODE = {0: (1.0e9, 2.5e9), 1: (3.0e9, 4.0e9), 2: (1.5e9, 2.0e9), 3: (0.4e9, 0.7e9)}
+
+
+@pytest.mark.parametrize("stage,budget", [(1, 200.0), (0, 200.0), (1, 1e9), (0, 1e9)])
+def test_x_regime_per_tile(stage, budget, tmp_path):
+    """Reading R32: tile t's table regime is 1 when staged; otherwise 3 when its x span (tw or
+    the remainder's columns, 4 bytes each) exceeds the L2 budget, 2 for the first tile, else 0.
+    Per-tile predicted time equals the transcription with that regime's table."""
+    from paper_1103_2405_b200 import Plan
+    ent = []
+    for mode, (prm, pcm) in PERF_MODE.items():
+        for valued in (0, 1):
+            for w in (1, 8, 64, 4096):
+                for h in (1, 32, 1024):
+                    ent += [[mode, valued, 0, w, h, prm], [mode, valued, 1, w, h, pcm]]
+    path = tmp_path / "modes.json"
+    path.write_text(json.dumps(dict(TABLE, l2_budget_bytes=budget, entries=ent)))
+    rp, col, _ = graphgen.random_csr(500, 700, 9000, seed=11, kind="powerlaw", valued=False)
+    tw, T, wl = 64, 3, 128
+    p = Plan(500, 700, rp, col, None, device=-1, tile_width=tw, num_tiles=T, workload_size=wl,
+             perf_table_path=str(path), stage_x=stage)
+    st = p.stats()
+    hists = tile_hists(500, 700, rp, col, tw, T)
+    for t in range(T + 1):
+        span = tw if t < T else 700 - T * tw
+        cached = bool(stage) and t < T
+        mode = 1 if cached else (3 if span * 4.0 > budget else (2 if t == 0 else 0))
+        prm, pcm = PERF_MODE[mode]
+        sec = model_ref.pm_packed(hists[t], wl, lambda k, w, h: prm if k == "rm" else pcm, TABLE["max_act_warp"])
+        rows = sum(c for _, c in hists[t])
+        us = sec * 1e6
+        if rows:
+            us += TABLE["launch_us"]
+            if cached:
+                us += tw * 4.0 * 148 / (TABLE["stage_GBps"] * 1e3)
+            if t > 0:
+                us += rows * 8.0 / (TABLE["rmw_GBps"] * 1e3)
+        assert math.isclose(st["tile_predicted_us"][t], us, rel_tol=1e-9), (t, mode, st["tile_predicted_us"][t], us)
