@@ -368,6 +368,14 @@ def main():
             extras["pagerank_dist_iterations"] = info["iterations"]
             extras["pagerank_dist_scaling"] = "strong (one graph over all ranks)"
             sd.close()
+            # the needed-columns exchange on the same graph
+            sn = pkg.Solver("pagerank", G.n, G.row_ptr, G.col, device=local, comm=comm, iter_kw=dict(exchange=1))
+            sn.run()
+            info = sn.run()
+            tt = torch.tensor([info["ms_total"]], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            extras["pagerank_dist_needed_iters_per_s"] = round(1e3 * info["iterations"] / float(tt.item()), 1)
+            sn.close()
             comm.close()
         except Exception as ex:          # reported, never fatal for the replica measurement
             extras["pagerank_dist_error"] = str(ex)[:300]
