@@ -202,6 +202,21 @@ spmv_status spmv_solver_create(int algo, int64_t n, int64_t m, const int64_t* ro
                                const int32_t* col, const spmv_iter_opts* it,
                                const spmv_options* opt, spmv_comm comm, int device,
                                spmv_solver* out);
+/* Row-partitioned solver from this rank's rows only (SURVEY 8(b) "*_local", for graphs too large
+ * to hold whole on every rank): the caller owns the vertices owned_ids[0 .. n_local) (every vertex
+ * of [0, n_global) owned by exactly one rank) and passes their rows of the iteration matrix with
+ * global column ids -- PageRank: the in-neighbours u of each owned v (edges u -> v, Eq. 6;
+ * duplicates already merged) plus out_degree[r] of each owned vertex; RWR: the neighbours in
+ * A u A^T (Eq. 9; reading R8), out_degree NULL (the row length is the degree).  Ownership
+ * and degrees of all vertices are exchanged once over the communicator (O(n) per rank); the
+ * iteration is the allgather path of spmv_solver_create with comm.  Results and runs as for
+ * spmv_solver_create (spmv_solver_result writes all n_global values on every rank).
+ * Errors: EINVAL (null pointer, HITS, PageRank without out_degree, overlapping / missing
+ * ownership, exchange = 1), ERANGE (id outside [0, n_global)), ENCCL, ECUDA. */
+spmv_status spmv_solver_create_local(int algo, int64_t n_global, int64_t n_local, const int32_t* owned_ids,
+                                     const int64_t* row_ptr, const int32_t* col, const int32_t* out_degree,
+                                     const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,
+                                     int device, spmv_solver* out);
 /* Run the power iteration from the initial vector (RWR: query node `query`).  Synchronises. */
 spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res);
 /* Copy the result to host, in the caller's vertex order: PageRank p [n], RWR r [n],

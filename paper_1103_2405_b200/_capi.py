@@ -77,6 +77,9 @@ SIGNATURES = {
     "spmv_needed_lists": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "spmv_plan_launches": (c_i32, [c_vp]),
     "spmv_iter_opts_default": (None, [ctypes.POINTER(IterOpts), ctypes.c_int]),
+    "spmv_solver_create_local": (c_i32, [ctypes.c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                                         ctypes.POINTER(IterOpts), ctypes.POINTER(Options), c_vp,
+                                         ctypes.c_int, ctypes.POINTER(c_vp)]),
     "spmv_solver_create": (c_i32, [ctypes.c_int, c_i64, c_i64, c_vp, c_vp, ctypes.POINTER(IterOpts),
                                    ctypes.POINTER(Options), c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     "spmv_solver_run": (c_i32, [c_vp, c_i64, c_vp, ctypes.POINTER(IterResult)]),

@@ -213,6 +213,28 @@ class Solver:
                                          ctypes.byref(h)), "spmv_solver_create")
         self._h = h
 
+    @classmethod
+    def local(cls, algo: str, n_global, owned_ids, row_ptr, col, out_degree=None, device=0, comm=None,
+              iter_kw=None, **options):
+        """Row-partitioned solver from this rank's rows only (spmv_solver_create_local)."""
+        self = cls.__new__(cls)
+        self.algo, self.n = algo, int(n_global)
+        self._comm = comm
+        ids = _np(owned_ids, np.int32)
+        rp = _np(row_ptr, np.int64)
+        cl = _np(col, np.int32)
+        deg = _np(out_degree, np.int32) if out_degree is not None else None
+        self.m = int(rp[-1]) if len(rp) else 0
+        self._it = iter_opts(algo, **(iter_kw or {}))
+        self._opt = make_options(**options)
+        h = ctypes.c_void_p()
+        check(C.lib().spmv_solver_create_local(ALGO[algo], self.n, len(ids), _ptr(ids), rp.ctypes.data, _ptr(cl),
+                                               _ptr(deg) if deg is not None else None, ctypes.byref(self._it),
+                                               ctypes.byref(self._opt), comm._h if comm is not None else None,
+                                               int(device), ctypes.byref(h)), "spmv_solver_create_local")
+        self._h = h
+        return self
+
     def run(self, query: int = 0, stream=None) -> dict:
         r = C.IterResult()
         st = C.lib().spmv_solver_run(self._h, int(query), _stream_handle(stream), ctypes.byref(r))

@@ -367,10 +367,27 @@ spmv_status exchange(spmv_comm c, Dist* D, const tc::Ctrl* ctrl, int sm_count, c
 }  // namespace
 
 
+// metadata allgather of the local-input variant (host vectors through device buffers, NCCL)
+static spmv_status allgather_host(spmv_comm c, const void* mine, void* all, size_t count, int dtype, size_t esize) {
+    if (c->world == 1) { std::memcpy(all, mine, count * esize); return SPMV_OK; }
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, count * esize * c->world);
+    if (e) return cuda_status(e, "metadata buffer");
+    spmv_status s = SPMV_OK;
+    e = cudaMemcpy((char*)d + (size_t)c->rank * count * esize, mine, count * esize, cudaMemcpyHostToDevice);
+    if (e) s = cuda_status(e, "metadata upload");
+    if (!s) s = nccl_status(g_nccl.AllGather((char*)d + (size_t)c->rank * count * esize, d, count, dtype, c->comm, nullptr),
+                            "ncclAllGather (metadata)");
+    if (!s && (e = cudaDeviceSynchronize())) s = cuda_status(e, "metadata allgather");
+    if (!s && (e = cudaMemcpy(all, d, count * esize * c->world, cudaMemcpyDeviceToHost))) s = cuda_status(e, "metadata download");
+    cudaFree(d);
+    return s;
+}
+
 spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* row_ptr,
                                const int32_t* col, const spmv_iter_opts* it,
                                const spmv_options* opt_in, spmv_comm comm, int device,
-                               spmv_solver* out) {
+                               spmv_solver* out, const LocalInput* li) {
     (void)m;
     cudaError_t e = cudaSetDevice(device);
     if (e) return cuda_status(e, "cudaSetDevice");
@@ -381,19 +398,59 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
     D->P = comm->world; D->rank = comm->rank;
     spmv_status st = SPMV_OK;
     try {
-        std::vector<int64_t> arp; std::vector<int32_t> acol;
-        clean_adjacency(n, row_ptr, col, arp, acol);
         std::vector<int64_t> mrp, len; std::vector<int32_t> mcol;
-        const int64_t nv = n;
-        n = build_iteration_matrix(algo, nv, arp, acol, mrp, mcol, len);   // n := vector length N
-        s->N = n;
-        // partition rows of M (bitonic over row lengths, Sec. 3.2)
-        std::vector<int64_t> rl(n);
-        for (int64_t i = 0; i < n; ++i) rl[i] = mrp[i + 1] - mrp[i];
-        std::vector<int32_t> owner(n);
-        std::vector<int64_t> lidx(n);
+        std::vector<int32_t> owner;
+        std::vector<int64_t> rl;                  // full input: row length of every vertex
+        std::vector<int64_t> in_row;              // local input: vertex -> input row (-1: not ours)
         int64_t S = 0;
-        if ((st = spmv_partition_plan(n, rl.data(), D->P, owner.data(), lidx.data(), &S))) throw st;
+        const int64_t nv = n;
+        if (!li) {
+            std::vector<int64_t> arp; std::vector<int32_t> acol;
+            clean_adjacency(n, row_ptr, col, arp, acol);
+            n = build_iteration_matrix(algo, nv, arp, acol, mrp, mcol, len);   // n := vector length N
+            // partition rows of M (bitonic over row lengths, Sec. 3.2)
+            rl.resize(n);
+            for (int64_t i = 0; i < n; ++i) rl[i] = mrp[i + 1] - mrp[i];
+            owner.resize(n);
+            std::vector<int64_t> lidx(n);
+            if ((st = spmv_partition_plan(n, rl.data(), D->P, owner.data(), lidx.data(), &S))) throw st;
+        } else {
+            // local input (SURVEY 8(b) "*_local"): this rank's rows only; ownership and the
+            // degrees of every vertex come from one metadata allgather (O(n) per rank, not O(m))
+            const int64_t nl = li->n_local;
+            std::vector<int64_t> counts(D->P);
+            if ((st = allgather_host(comm, &nl, counts.data(), 1, 4 /*ncclInt64*/, 8))) throw st;
+            const int64_t mx = *std::max_element(counts.begin(), counts.end());
+            S = mx;
+            std::vector<int32_t> mine(2 * std::max<int64_t>(mx, 1), -1), all(2 * std::max<int64_t>(mx, 1) * D->P);
+            for (int64_t r = 0; r < nl; ++r) {
+                mine[r] = li->owned[r];
+                mine[mx + r] = li->out_degree ? li->out_degree[r]
+                                              : (int32_t)(li->row_ptr[r + 1] - li->row_ptr[r]);
+            }
+            if ((st = allgather_host(comm, mine.data(), all.data(), 2 * std::max<int64_t>(mx, 1), 2 /*ncclInt32*/, 4))) throw st;
+            owner.assign(n, -1);
+            len.assign(n, 0);
+            const int64_t w = 2 * std::max<int64_t>(mx, 1);
+            for (int32_t q = 0; q < D->P; ++q)
+                for (int64_t r = 0; r < counts[q]; ++r) {
+                    const int32_t v = all[q * w + r];
+                    if (v < 0 || v >= n || owner[v] != -1) { set_error("owned ids overlap or out of range"); throw SPMV_EINVAL; }
+                    owner[v] = q;
+                    len[v] = all[q * w + mx + r];
+                }
+            for (int64_t v = 0; v < n; ++v)
+                if (owner[v] < 0) { set_error("a vertex is owned by no rank"); throw SPMV_EINVAL; }
+            in_row.assign(n, -1);
+            for (int64_t r = 0; r < nl; ++r) in_row[li->owned[r]] = r;
+        }
+        s->N = n;
+        auto row_len = [&](int64_t v) -> int64_t {
+            return li ? li->row_ptr[in_row[v] + 1] - li->row_ptr[in_row[v]] : rl[v];
+        };
+        auto row_cols = [&](int64_t v) -> const int32_t* {
+            return li ? li->col + li->row_ptr[in_row[v]] : mcol.data() + mrp[v];
+        };
         // Exchange only globally non-empty columns: for PageRank / RWR a column of
         // the iteration matrix is empty exactly when the vertex has no out-edges (inv = 0), so its
         // z is never read.  On each rank the non-empty rows come first (ascending id), then the
@@ -419,15 +476,20 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
             if (owner[i] == D->rank) D->owned[D->lrow[i]] = (int32_t)i;
         }
         D->n_local = (int64_t)D->owned.size();
-        // local rows (ascending vertex id = local index order), original column ids
+        // local rows (lrow order: non-empty columns first, each part by ascending id), global ids
         std::vector<int64_t> lrp(D->n_local + 1, 0);
-        for (int64_t r = 0; r < D->n_local; ++r) lrp[r + 1] = lrp[r] + rl[D->owned[r]];
+        for (int64_t r = 0; r < D->n_local; ++r) lrp[r + 1] = lrp[r] + row_len(D->owned[r]);
         std::vector<int32_t> lcol(lrp[D->n_local]);
         std::vector<char> seen(n, 0);
         for (int64_t r = 0; r < D->n_local; ++r) {
             const int64_t v = D->owned[r];
-            std::copy(mcol.begin() + mrp[v], mcol.begin() + mrp[v + 1], lcol.begin() + lrp[r]);
-            for (int64_t k = mrp[v]; k < mrp[v + 1]; ++k) seen[mcol[k]] = 1;
+            const int32_t* c = row_cols(v);
+            const int64_t L = row_len(v);
+            for (int64_t k = 0; k < L; ++k) {
+                if (c[k] < 0 || c[k] >= n) { set_error("column out of range"); throw SPMV_EINVAL; }
+                lcol[lrp[r] + k] = c[k];
+                seen[c[k]] = 1;
+            }
         }
         for (int64_t j = 0; j < n; ++j) D->nzc += seen[j];
         spmv_options opt;
@@ -440,6 +502,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         std::vector<int64_t> part_off(D->P);
         int64_t g_floats = (int64_t)D->P * D->slot;
         D->exchange = s->it.exchange == 1;
+        if (D->exchange && li) { set_error("exchange = 1 needs the full graph on every rank"); throw SPMV_EINVAL; }
         if (!D->exchange) {
             for (int64_t k = 0; k < D->nzc; ++k) {
                 idx[k] = (int32_t)D->gpos[p->perm[k]];

@@ -225,6 +225,29 @@ spmv_status spmv_solver_create(int algo, int64_t n, int64_t m, const int64_t* ro
 }
 
 __attribute__((visibility("default")))
+spmv_status spmv_solver_create_local(int algo, int64_t n_global, int64_t n_local, const int32_t* owned_ids,
+                                     const int64_t* row_ptr, const int32_t* col, const int32_t* out_degree,
+                                     const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,
+                                     int device, spmv_solver* out) {
+    if (!out || !comm || n_global < 1 || n_local < 0 || (n_local > 0 && (!owned_ids || !row_ptr)) ||
+        (n_local > 0 && row_ptr[n_local] > 0 && !col)) {
+        set_error("invalid argument"); return SPMV_EINVAL;
+    }
+    if (algo != SPMV_ALGO_PAGERANK && algo != SPMV_ALGO_RWR) { set_error("local input: PageRank or RWR"); return SPMV_EINVAL; }
+    if (algo == SPMV_ALGO_PAGERANK && n_local > 0 && !out_degree) { set_error("PageRank needs out_degree"); return SPMV_EINVAL; }
+    if (n_local > 0 && row_ptr[0] != 0) { set_error("row_ptr[0] != 0"); return SPMV_EINVAL; }
+    for (int64_t i = 0; i < n_local; ++i) {
+        if (row_ptr[i + 1] < row_ptr[i]) { set_error("row_ptr not monotone"); return SPMV_EINVAL; }
+        if (owned_ids[i] < 0 || owned_ids[i] >= n_global) { set_error("owned id out of range"); return SPMV_ERANGE; }
+        if (out_degree && out_degree[i] < 0) { set_error("negative degree"); return SPMV_EINVAL; }
+    }
+    if (device < 0) { set_error("solvers need a device"); return SPMV_EINVAL; }
+    LocalInput li{n_local, owned_ids, row_ptr, col, out_degree};
+    return solver_create_dist(algo, n_global, n_local > 0 ? row_ptr[n_local] : 0, nullptr, nullptr, it, opt, comm,
+                              device, out, &li);
+}
+
+__attribute__((visibility("default")))
 spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res) {
     if (!s) { set_error("null solver"); return SPMV_EINVAL; }
     if (s->comm) return solver_run_dist(s, query, stream, res);

@@ -65,10 +65,17 @@ struct spmv_solver_s {
 };
 
 // multi-GPU row-partitioned solvers (dist.cu)
+struct LocalInput {                 // spmv_solver_create_local: this rank's rows only
+    int64_t n_local;
+    const int32_t* owned;           // [n_local] global vertex ids
+    const int64_t* row_ptr;         // [n_local + 1] rows of the iteration matrix
+    const int32_t* col;             // global column ids
+    const int32_t* out_degree;      // [n_local] (PageRank); NULL: the row length (RWR)
+};
 spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* row_ptr,
                                const int32_t* col, const spmv_iter_opts* it,
                                const spmv_options* opt, spmv_comm comm, int device,
-                               spmv_solver* out);
+                               spmv_solver* out, const LocalInput* li = nullptr);
 spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res);
 spmv_status solver_result_dist(spmv_solver s, float* out0, float* out1);
 void solver_destroy_dist(spmv_solver s);

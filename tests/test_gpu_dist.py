@@ -78,3 +78,55 @@ def test_dist_needed_exchange_world1(algo, gpu):
         a, h = s.result()
         ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=1, fixed_iters=info["iterations"])
         assert np.abs(a - ra).sum() < 1e-6 and np.abs(h - rh).sum() < 1e-6, info
+
+
+def _sym_rows(G):
+    """rows of A u A^T (RWR's graph, reading R8) as CSR over all vertices."""
+    u = (G.keys >> np.uint64(32)).astype(np.int64)
+    v = (G.keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    a = np.concatenate([u, v])
+    b = np.concatenate([v, u])
+    key = np.unique(a * G.n + b)
+    a, b = key // G.n, key % G.n
+    rp = np.concatenate([[0], np.cumsum(np.bincount(a, minlength=G.n))]).astype(np.int64)
+    return rp, b.astype(np.int32)
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "rwr"])
+def test_local_input_world1(algo, gpu):
+    """spmv_solver_create_local (SURVEY 8(b) "*_local"): the rank passes only its rows (here all,
+    in a shuffled order) of the iteration matrix with global ids; parity with the oracle."""
+    from paper_1103_2405_b200 import Solver
+    G = graphgen.make_graph("t_small")
+    if algo == "pagerank":
+        rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)     # in-neighbours
+        deg = np.diff(G.row_ptr).astype(np.int32)
+    else:
+        rp, col = _sym_rows(G)
+        deg = None
+    order = np.random.default_rng(3).permutation(G.n).astype(np.int32)
+    lens = np.diff(rp)[order]
+    lrp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    lcol = np.concatenate([col[rp[v]:rp[v + 1]] for v in order]).astype(np.int32)
+    s = Solver.local(algo, G.n, order, lrp, lcol, out_degree=None if deg is None else deg[order],
+                     device=0, comm=comm1())
+    q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][3])
+    info = s.run(q) if algo == "rwr" else s.run()
+    if algo == "pagerank":
+        ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
+    else:
+        ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, q, fixed_iters=info["iterations"])
+    assert np.abs(s.result().astype(np.float64) - ref).sum() < 1e-6, info
+
+
+def test_local_input_errors(gpu):
+    from paper_1103_2405_b200 import Solver, SpmvError
+    G = graphgen.make_graph("t_small")
+    rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)
+    ids = np.arange(G.n, dtype=np.int32)
+    with pytest.raises(SpmvError):                     # PageRank without degrees
+        Solver.local("pagerank", G.n, ids, rp, col, device=0, comm=comm1())
+    with pytest.raises(SpmvError):                     # HITS is not a local-input algorithm
+        Solver.local("hits", G.n, ids, rp, col, device=0, comm=comm1())
+    with pytest.raises(SpmvError):                     # a vertex owned by nobody
+        Solver.local("rwr", G.n, ids[:-1], rp[:-1], col[:rp[-2]], device=0, comm=comm1())
