@@ -44,6 +44,7 @@ __device__ __forceinline__ void st_last(float* a, float v, uint64_t pol) {
 #ifndef PB_RT
 #define PB_RT 512
 #endif
+__device__ const uint16_t* g_rid;                          // PB_FLAT == 2: run index per stage position
 template <bool VALUED>
 __global__ void __launch_bounds__(PB_ET, 2) pb_expand(const Chunk* __restrict__ chunks, const Run* __restrict__ runs,
                                                       const uint32_t* __restrict__ cd, const float* __restrict__ val,
@@ -86,7 +87,13 @@ __global__ void __launch_bounds__(PB_ET, 2) pb_expand(const Chunk* __restrict__ 
     // runs (sorted by stage start) are found with one ballot-free step per 32 positions: lanes hold
     // a window of 32 run descriptors; runs starting inside the step set bits of a mask (redux.or),
     // and lane i's run is the window base + popc(mask & lanes <= i) - 1 (+ the run open at q0)
-#if PB_FLAT
+#if PB_FLAT == 2
+    // static run index of every stage position (2 B, coalesced): destination without a search
+    for (int q = threadIdx.x; q < c.n; q += PB_ET) {
+        const int r = __ldcs(g_rid + c.e0 + q);
+        st_last(buf + rg[r] + (q - rs[r]), stage[q], pol);
+    }
+#elif PB_FLAT
     const int L = ((c.n + PB_ET / 32 - 1) / (PB_ET / 32) + 31) & ~31;   // positions per warp (multiple of 32)
     const int q_beg = warp * L, q_end = min(c.n, q_beg + L);
     if (q_beg < q_end) {
@@ -298,6 +305,7 @@ __global__ void __launch_bounds__(PB_RT, 1) pb_reduce_pipe(const Bin* __restrict
 }
 
 extern "C" {
+int pb_set_rid(const uint16_t* rid) { return (int)cudaMemcpyToSymbol(g_rid, &rid, sizeof(rid)); }
 int pb_setup(int stage_bytes, int region_bytes) {
     cudaError_t e = cudaFuncSetAttribute(pb_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
     if (!e) e = cudaFuncSetAttribute(pb_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);

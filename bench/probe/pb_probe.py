@@ -92,6 +92,9 @@ def build(rp, col, n, G=4, C=8192, RB=24576, RROWS=8192, WMAX=64):
     gpos = gpos - bs0[b1] + rs_pad[b1]
     runs["goff"] = gpos[first] - gbase[g1[first]]
     run_ch = ch_of[first]
+    # run index (within its chunk) of every stage position, chunk-major (PB_FLAT == 2)
+    run_of_t = np.searchsorted(rstart, np.arange(m), "right") - 1
+    rid = (run_of_t - np.searchsorted(run_ch, ch_of[o2], "left")).astype(np.uint16)
     chunks = np.zeros(nch, CHUNK_DT)
     chunks["e0"] = cs[:-1]
     chunks["n"] = np.diff(cs)
@@ -155,7 +158,7 @@ def build(rp, col, n, G=4, C=8192, RB=24576, RROWS=8192, WMAX=64):
     info = dict(m=m, n=n, G=G, chunks=nch, runs=len(runs), bins=nb, slabs=S, npos=npos,
                 mean_run=round(m / max(len(runs), 1), 1), max_group_entries=int(np.diff(gbase).max()),
                 build_s=round(time.time() - t0, 1))
-    return dict(cd=cd, perm_val=perm_val, nlen=nlen.astype(np.int32), rcum=cum.astype(np.int64), chunks=chunks, runs=runs, gc=gc, gb=gb, bins=bins, slabs=slabs,
+    return dict(rid=rid, cd=cd, perm_val=perm_val, nlen=nlen.astype(np.int32), rcum=cum.astype(np.int64), chunks=chunks, runs=runs, gc=gc, gb=gb, bins=bins, slabs=slabs,
                 pos=pos, rperm=rperm, ge=ge, info=info)
 
 
@@ -221,7 +224,9 @@ def main():
     stage_b, region_b = 4 * int(os.environ.get("PB_C", 8192)) + 12 * int(T["chunks"]["nrun"].max()) + 16, 4 * (T["bins"]["rlen"].max() + 12) + (2 * int(T["bins"]["plen"].max()) + 64 if os.environ.get("PB_POS_SMEM") == "1" else 0)
     assert lib.pb_setup(stage_b, int(region_b)) == 0
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).cuda()
-    d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "rcum")}
+    d = {k: dev(T[k]) for k in ("cd", "chunks", "runs", "bins", "slabs", "pos", "rcum", "rid")}
+    if hasattr(lib, "pb_set_rid"):
+        assert lib.pb_set_rid(ctypes.c_void_p(d["rid"].data_ptr())) == 0
     dv = torch.from_numpy(val_o1).cuda() if val_o1 is not None else None
     xt = torch.from_numpy(x).cuda()
     stride = (T["info"]["max_group_entries"] + 16 + 63) // 64 * 64
