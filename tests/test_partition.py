@@ -270,3 +270,75 @@ def test_gloo_pagerank_needed_exchange(world, tmp_path):
     for r in range(world):
         p = np.load(tmp_path / f"p{r}.npy")
         assert np.abs(p - ref).sum() < 1e-12
+
+
+def _worker_hits(rank, world, port, result_dir, iters, norm):
+    """The row-partitioned HITS protocol of csrc/dist.cu in fp64: rows of the block matrix
+    [[0, A^T], [A, 0]] dealt by the bitonic partition; every exchange carries the raw product y of
+    a rank's rows plus its half sums and the L1 change of its previous normalisation; every rank
+    sums the partials in rank order, normalises its own rows and the gathered x itself, and the
+    stop decision lags one SpMV (reading R14: compared at the oracle's iteration count)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1103_2405_b200 import partition_plan
+    G = graphgen.make_graph("t_small")
+    n = G.n
+    src = np.repeat(np.arange(n), np.diff(G.row_ptr))
+    dst = G.col.astype(np.int64)
+    N = 2 * n
+    # block rows: v < n (authority) reads h_u = x[n + u] for u -> v; n + u (hub) reads a_v = x[v]
+    rows = np.concatenate([dst, n + src])
+    cols = np.concatenate([n + src, dst])
+    rl = np.bincount(rows, minlength=N)
+    owner, _, _ = partition_plan(rl, world)
+    mine = np.nonzero(owner == rank)[0]
+    sel = owner[rows] == rank
+    half = (np.arange(N) >= n).astype(np.int64)
+    x = np.full(N, 1.0 / n)                      # a(0) = h(0) = 1/|V| (L440)
+    v_old = np.full(N, 1.0 / n)
+    res_own, it = 0.0, 0
+    while True:
+        y = np.bincount(rows[sel], weights=x[cols[sel]], minlength=N)[mine]      # own rows, raw
+        d = np.abs(y) if norm == 1 else y * y
+        part = np.array([d[half[mine] == 0].sum(), d[half[mine] == 1].sum(), res_own])
+        slot = np.zeros(N)
+        slot[mine] = y
+        ys = [torch.zeros(N, dtype=torch.float64) for _ in range(world)]
+        ps = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(ys, torch.from_numpy(slot))
+        dist.all_gather(ps, torch.from_numpy(part))
+        tot = np.zeros(3)
+        for q in range(world):                                                   # rank order
+            tot += ps[q].numpy()
+        if it >= 1 and it >= iters:                                              # lagged stop
+            break
+        nrm = tot[:2] if norm == 1 else np.sqrt(tot[:2])
+        yall = sum(t.numpy() for t in ys)
+        scale = np.where(nrm[half] > 0, 1.0 / np.where(nrm[half] > 0, nrm[half], 1.0), 0.0)
+        uni = 1.0 / n if norm == 1 else 1.0 / np.sqrt(n)
+        x = np.where(nrm[half] > 0, yall * scale, uni)                          # gathered x, normalised
+        v_new = x[mine]
+        res_own = float(np.abs(v_new - v_old[mine]).sum())
+        v_old[mine] = v_new
+        it += 1
+    parts = [None] * world
+    dist.all_gather_object(parts, (mine.tolist(), v_old[mine].tolist()))
+    full = np.zeros(N)
+    for rws, vals in parts:
+        full[rws] = vals
+    np.save(os.path.join(result_dir, f"h{rank}.npy"), full)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,norm", [(2, 1), (3, 2)])
+def test_gloo_hits_protocol(world, norm, tmp_path):
+    iters = 10
+    port = _free_port()
+    mp.spawn(_worker_hits, args=(world, port, str(tmp_path), iters, norm), nprocs=world, join=True)
+    G = graphgen.make_graph("t_small")
+    ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=norm, fixed_iters=iters)
+    for r in range(world):
+        v = np.load(tmp_path / f"h{r}.npy")
+        assert np.abs(v[:G.n] - ra).sum() < 1e-12 and np.abs(v[G.n:] - rh).sum() < 1e-12
