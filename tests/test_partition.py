@@ -342,3 +342,54 @@ def test_gloo_hits_protocol(world, norm, tmp_path):
     for r in range(world):
         v = np.load(tmp_path / f"h{r}.npy")
         assert np.abs(v[:G.n] - ra).sum() < 1e-12 and np.abs(v[G.n:] - rh).sum() < 1e-12
+
+
+def _worker_rwr(rank, world, port, result_dir, iters, q):
+    """The row-partitioned RWR protocol (Eq. 9, readings R6-R8) in fp64: rows of W = A_sym D^-1
+    by the bitonic partition of A_sym's rows; each rank exchanges z = r / deg of its own vertices
+    (allgather of slots) plus its L1 change; r' = c (A_sym z) + (1 - c) e_q on its own rows."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1103_2405_b200 import partition_plan
+    G = graphgen.make_graph("t_small")
+    n, c = G.n, 0.9
+    u = np.repeat(np.arange(n), np.diff(G.row_ptr))
+    v = G.col.astype(np.int64)
+    key = np.unique(np.concatenate([u * n + v, v * n + u]))                   # A u A^T, merged
+    rows, cols = key // n, key % n
+    deg = np.bincount(rows, minlength=n).astype(np.float64)
+    owner, _, _ = partition_plan(deg.astype(np.int64), world)
+    mine = np.nonzero(owner == rank)[0]
+    sel = owner[rows] == rank
+    inv = np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0.0)
+    r = np.zeros(n)
+    r[q] = 1.0                                                                # r(0) = e_q (R7)
+    for _ in range(iters):
+        slot = np.zeros(n)
+        slot[mine] = r[mine] * inv[mine]
+        zs = [torch.zeros(n, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(zs, torch.from_numpy(slot))
+        z = sum(t.numpy() for t in zs)
+        y = np.bincount(rows[sel], weights=z[cols[sel]], minlength=n)[mine]
+        rn = c * y + (1 - c) * (mine == q)
+        r[mine] = rn
+    parts = [None] * world
+    dist.all_gather_object(parts, (mine.tolist(), r[mine].tolist()))
+    full = np.zeros(n)
+    for rws, vals in parts:
+        full[rws] = vals
+    np.save(os.path.join(result_dir, f"r{rank}.npy"), full)
+    dist.destroy_process_group()
+
+
+def test_gloo_rwr_protocol(tmp_path):
+    world, iters = 2, 15
+    G = graphgen.make_graph("t_small")
+    q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][3])
+    port = _free_port()
+    mp.spawn(_worker_rwr, args=(world, port, str(tmp_path), iters, q), nprocs=world, join=True)
+    ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, q, fixed_iters=iters)
+    for rk in range(world):
+        assert np.abs(np.load(tmp_path / f"r{rk}.npy") - ref).sum() < 1e-12
