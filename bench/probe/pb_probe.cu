@@ -273,7 +273,10 @@ __device__ __forceinline__ void reduce_bin(const Bin& b, const Slab* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(PB_RT, 1) pb_reduce_pipe(const Bin* __restrict__ bins, int nbins, int buf_floats,
+#ifndef PB_PIPE_CTAS
+#define PB_PIPE_CTAS 1
+#endif
+__global__ void __launch_bounds__(PB_RT, PB_PIPE_CTAS) pb_reduce_pipe(const Bin* __restrict__ bins, int nbins, int buf_floats,
                                                        const Slab* __restrict__ slabs, const uint16_t* __restrict__ pos,
                                                        const int64_t* __restrict__ rcum, const float* __restrict__ buf,
                                                        float* __restrict__ y) {
@@ -349,7 +352,7 @@ int pb_run(int G, int phases, const int32_t* gc, const int32_t* gb, const void* 
                     static int sms = 0;
                     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
                     const int bf = ((region_bytes / 4) + 31) & ~31;
-                    pb_reduce_pipe<<<nb < sms ? nb : sms, PB_RT, 2 * bf * 4, s2>>>((const Bin*)bins + gb[g], nb, bf,
+                    pb_reduce_pipe<<<nb < PB_PIPE_CTAS * sms ? nb : PB_PIPE_CTAS * sms, PB_RT, 2 * bf * 4, s2>>>((const Bin*)bins + gb[g], nb, bf,
                                                                                   (const Slab*)slabs, pos, rcum, b, y);
                 } else {
                     pb_reduce<<<nb, PB_RT, region_bytes, s2>>>((const Bin*)bins + gb[g], (const Slab*)slabs, pos, rcum, b, y);
