@@ -397,6 +397,7 @@ def main():
             "gpu_launches": int(args.steps * nl),
             "clocks": clk.summary(t0, t1),
             "predicted_us": round(st["predicted_us"], 2),
+            "plan_build_ms": round(st["build_ms"], 1),      # one-time, amortised, not in the step
             "batches_ms_per_step": {"n": nb, "median": round(float(np.median(batch_ms)), 5),
                                     "mean": round(float(np.mean(batch_ms)), 5)},
         }
