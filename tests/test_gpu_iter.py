@@ -181,3 +181,32 @@ def test_config1_c2_full_size(algo, gpu):
         assert np.abs(s.result().astype(np.float64) - ref).sum() < L1_BAR, info
     assert info["converged"]
     s.close()
+
+
+@pytest.mark.parametrize("alpha", [1.8, 2.6])
+def test_config2_c3_skew_sweep_full_size(alpha, gpu):
+    """BASELINE configs[2] (Flickr-shaped capped Chung-Lu, 1.7 M vertices, 22.6 M edges) at the two
+    ends of the power-law sweep, auto-tuned plans: PageRank within 1e-6 L1 of the oracle at equal
+    k, and the valued SpMV on sampled rows (random + the 50 longest) within the per-element bar."""
+    import torch
+    from paper_1103_2405_b200 import Plan, Solver
+    G = graphgen.make_graph("c3_flickr", alpha=alpha)
+    s = Solver("pagerank", G.n, G.row_ptr, G.col, device=0)
+    info = s.run()
+    ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
+    assert info["converged"] and np.abs(s.result().astype(np.float64) - ref).sum() < L1_BAR, info
+    s.close()
+    val = graphgen.edge_values(G.keys)
+    x = graphgen.uniform_f32(G.n, seed=graphgen.SEED_X)
+    p = Plan(G.n, G.n, G.row_ptr, G.col, val, device=0)
+    yt = torch.empty(G.n, device="cuda")
+    p.execute(torch.from_numpy(x).cuda(), yt)
+    torch.cuda.synchronize()
+    y = yt.cpu().numpy().astype(np.float64)
+    lens = np.diff(G.row_ptr)
+    rows = np.unique(np.concatenate([np.random.default_rng(1).choice(G.n, 2000, replace=False),
+                                     np.argsort(-lens)[:50]]))
+    sub_rp = np.concatenate([[0], np.cumsum(lens[rows])]).astype(np.int64)
+    idx = np.concatenate([np.arange(G.row_ptr[r], G.row_ptr[r + 1]) for r in rows])
+    yo, bo = oracle.spmv(sub_rp, G.col[idx], val[idx], x)
+    assert np.all(np.abs(y[rows] - yo) <= 1e-5 * bo + 1e-30)
