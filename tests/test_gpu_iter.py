@@ -183,14 +183,14 @@ def test_config1_c2_full_size(algo, gpu):
     s.close()
 
 
-@pytest.mark.parametrize("alpha", [1.8, 2.6])
-def test_config2_c3_skew_sweep_full_size(alpha, gpu):
-    """BASELINE configs[2] (Flickr-shaped capped Chung-Lu, 1.7 M vertices, 22.6 M edges) at the two
-    ends of the power-law sweep, auto-tuned plans: PageRank within 1e-6 L1 of the oracle at equal
+@pytest.mark.parametrize("cfg,alpha", [("c3_flickr", 1.8), ("c3_flickr", 2.6), ("c3_youtube", 2.2)])
+def test_config2_c3_skew_sweep_full_size(cfg, alpha, gpu):
+    """BASELINE configs[2] (Flickr-shaped capped Chung-Lu, 1.7 M vertices, 22.6 M edges, at the two
+    ends of the power-law sweep; YouTube-shaped, 1.1 M / 4.9 M), auto-tuned plans: PageRank within 1e-6 L1 of the oracle at equal
     k, and the valued SpMV on sampled rows (random + the 50 longest) within the per-element bar."""
     import torch
     from paper_1103_2405_b200 import Plan, Solver
-    G = graphgen.make_graph("c3_flickr", alpha=alpha)
+    G = graphgen.make_graph(cfg, alpha=alpha)
     s = Solver("pagerank", G.n, G.row_ptr, G.col, device=0)
     info = s.run()
     ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
