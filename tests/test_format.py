@@ -215,3 +215,18 @@ def test_export_file_matches_format_oracle(tmp_path, valued):
     else:
         assert "slot_val" not in E
     assert np.array_equal(E["split"].reshape(-1, 3), ref.split.reshape(-1, 3))
+
+
+def test_plain_c_consumer(tmp_path):
+    """The boundary is a C ABI: a C99 program compiled against include/spmv.h and linked to
+    libtcspmv.so (no Python, no torch) partitions, builds a host-only plan and decodes it."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1103_2405_b200", "lib")
+    exe = str(tmp_path / "abi_consumer")
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "c", "abi_consumer.c"), "-L", libdir, "-ltcspmv",
+                        "-Wl,-rpath," + libdir, "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
