@@ -188,3 +188,33 @@ def test_permute_scatter_equals_gather(gpu, monkeypatch):
         p.close()
     assert out[0].tobytes() == out[1].tobytes()
     check(out[0], rp, col, val, x.cpu().numpy())
+
+
+def test_plain_c_consumer_on_gpu(gpu, tmp_path):
+    """The whole path through the C ABI from a C99 program (no Python/torch on the path): valued
+    SpMV via spmv_execute_host and the one-shot pagerank(), checked against the fp64 oracle."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1103_2405_b200", "lib")
+    exe = str(tmp_path / "abi_gpu_consumer")
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "c", "abi_gpu_consumer.c"), "-L", libdir, "-ltcspmv",
+                        "-Wl,-rpath," + libdir, "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    G = graphgen.make_graph("t_mid")
+    rp, col = graphgen.keys_to_csr(G.keys, G.n, transpose=True)
+    val = graphgen.edge_values(G.keys[np.lexsort((G.keys >> np.uint64(32), G.keys & np.uint64(0xFFFFFFFF)))])
+    x = graphgen.uniform_f32(G.n, seed=3)
+    for name, arr in (("rp", rp.astype(np.int64)), ("col", col.astype(np.int32)), ("val", val.astype(np.float32)),
+                      ("x", x), ("grp", G.row_ptr.astype(np.int64)), ("gcol", G.col.astype(np.int32))):
+        arr.tofile(str(tmp_path / f"{name}.bin"))
+    r = subprocess.run([exe, str(tmp_path), str(G.n), str(len(col)), str(len(G.col))], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    y = np.fromfile(str(tmp_path / "y.bin"), np.float32)
+    check(y, rp, col, val, x)
+    k = int(r.stdout.strip())
+    p = np.fromfile(str(tmp_path / "p.bin"), np.float32).astype(np.float64)
+    ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=k)
+    assert np.abs(p - ref).sum() < 1e-6
