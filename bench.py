@@ -48,7 +48,36 @@ class ClockSampler:
         self.index, self.samples, self.stop = index, [], threading.Event()
         self.marks = []
 
+    def _nvml(self):
+        """NVML (what nvidia-smi reads) polled every 5 ms: enough samples inside a sub-second timed
+        region; the device is matched by PCI bus id (CUDA and NVML orderings may differ)."""
+        try:
+            import pynvml as N
+            import torch
+            N.nvmlInit()
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception:
+            return False
+        bits = [0x8, 0x40, 0x20, 0x4]     # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = get_reasons(h)
+                flags = ",".join("Active" if r & b else "Not Active" for b in bits)
+                self.samples.append((time.time(), f"{sm}, {mx}, {flags}"))
+            except Exception:
+                pass
+            time.sleep(0.005)
+        return True
+
     def _run(self):
+        if self._nvml():
+            return
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
