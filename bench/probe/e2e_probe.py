@@ -15,11 +15,11 @@ G = graphgen.make_graph("c2")
 val = graphgen.edge_values(G.keys)
 x = graphgen.uniform_f32(G.n, seed=3)
 plan = pkg.Plan(G.n, G.n, G.row_ptr, G.col, val, device=0)
-stream = torch.cuda.current_stream()
-for cnt in (8, 32, 64):
+streams = {"default": torch.cuda.current_stream(), "side": torch.cuda.Stream()}
+for (sname, stream), cnt in [(kv, c) for kv in streams.items() for c in (32,)]:
     xh = torch.from_numpy(x).unsqueeze(0).expand(cnt, G.n).contiguous().pin_memory()
     yh = torch.empty((cnt, G.n), dtype=torch.float32).pin_memory()
-    for pipe in ("2", "3"):
+    for pipe in ("3",):
         os.environ["TCSPMV_PIPE"] = pipe
         call = lambda c: pkg._capi.check(pkg.lib().spmv_execute_host_batch(
             plan._h, ctypes.c_void_p(xh.data_ptr()), ctypes.c_void_p(yh.data_ptr()), c,
@@ -33,4 +33,4 @@ for cnt in (8, 32, 64):
             e1.record(stream)
             torch.cuda.synchronize()
             res.append(e0.elapsed_time(e1) / cnt)
-        print(json.dumps(dict(count=cnt, pipe=int(pipe), ms_per_step=[round(r, 4) for r in res])), flush=True)
+        print(json.dumps(dict(stream=sname, count=cnt, pipe=int(pipe), ms_per_step=[round(r, 4) for r in res])), flush=True)
