@@ -101,28 +101,63 @@ static inline int32_t tile_of(int64_t k, int64_t tw, int32_t T) {
     return t < T ? (int32_t)t : T;
 }
 
-void tile_histograms(const Prepared& P, int64_t tw, int32_t T,
-                     std::vector<std::vector<std::pair<int64_t, int64_t>>>& hist) {
-    hist.assign(T + 1, {});
-    int64_t cap = P.max_row_len + 1;
-    // per tile dense histogram over [0, cap) (tiles are few; cap = longest row + 1)
-    std::vector<std::vector<int64_t>> h(T + 1, std::vector<int64_t>(cap, 0));
+// Row-length histograms of every tile for several tile counts at one tile width, in one pass over
+// the entries (the auto-tuner evaluates all candidate counts of a width).  Thread-local dense
+// counters for lengths below kSmall, atomics only for the rare longer segments.
+void tile_histograms_multi(const Prepared& P, int64_t tw, const std::vector<int32_t>& Ts,
+                           std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>>& out) {
+    constexpr int64_t kSmall = 4096;
+    const size_t J = Ts.size();
+    int32_t Tmax = 0;
+    for (int32_t T : Ts) Tmax = std::max(Tmax, T);
+    std::vector<size_t> base(J + 1, 0);                     // flat (j, t) slot index
+    for (size_t j = 0; j < J; ++j) base[j + 1] = base[j] + (size_t)Ts[j] + 1;
+    const size_t S = base[J];
+    const int64_t cap = P.max_row_len + 1;
+    std::vector<std::vector<int64_t>> big(S, std::vector<int64_t>(cap > kSmall ? cap : 0, 0));
+    std::vector<int64_t> small(S * kSmall, 0);
     #pragma omp parallel
     {
-        std::vector<int64_t> seg(T + 1);
-        #pragma omp for schedule(dynamic, 1024)
+        std::vector<int64_t> loc(S * kSmall, 0);
+        std::vector<int64_t> seg(Tmax + 1);
+        auto add = [&](size_t slot, int64_t len) {
+            if (len < kSmall) loc[slot * kSmall + len]++;
+            else __atomic_fetch_add(&big[slot][len], 1, __ATOMIC_RELAXED);
+        };
+        #pragma omp for schedule(dynamic, 4096)
         for (int64_t i = 0; i < P.n_rows; ++i) {
-            int64_t s = P.rp[i], e = P.rp[i + 1];
-            if (s == e) { __atomic_fetch_add(&h[T][0], 1, __ATOMIC_RELAXED); continue; }
+            const int64_t s = P.rp[i], e = P.rp[i + 1];
+            if (s == e) { for (size_t j = 0; j < J; ++j) add(base[j] + Ts[j], 0); continue; }
             std::fill(seg.begin(), seg.end(), 0);
-            for (int64_t p = s; p < e; ++p) seg[tile_of(P.kcol[p], tw, T)]++;
-            for (int32_t t = 0; t <= T; ++t)
-                if (seg[t]) __atomic_fetch_add(&h[t][seg[t]], 1, __ATOMIC_RELAXED);
+            for (int64_t p = s; p < e; ++p) seg[tile_of(P.kcol[p], tw, Tmax)]++;
+            for (size_t j = 0; j < J; ++j) {
+                int64_t used = 0;
+                for (int32_t t = 0; t < Ts[j]; ++t)
+                    if (seg[t]) { add(base[j] + t, seg[t]); used += seg[t]; }
+                if (e - s - used) add(base[j] + Ts[j], e - s - used);
+            }
+        }
+        #pragma omp critical
+        for (size_t k = 0; k < loc.size(); ++k) small[k] += loc[k];
+    }
+    out.assign(J, {});
+    for (size_t j = 0; j < J; ++j) {
+        out[j].assign(Ts[j] + 1, {});
+        for (int32_t t = 0; t <= Ts[j]; ++t) {
+            const size_t slot = base[j] + t;
+            for (int64_t l = cap - 1; l >= kSmall; --l)
+                if (big[slot][l]) out[j][t].push_back({l, big[slot][l]});
+            for (int64_t l = std::min<int64_t>(cap, kSmall) - 1; l >= 0; --l)
+                if (small[slot * kSmall + l]) out[j][t].push_back({l, small[slot * kSmall + l]});
         }
     }
-    for (int32_t t = 0; t <= T; ++t)
-        for (int64_t l = cap - 1; l >= 0; --l)
-            if (h[t][l]) hist[t].push_back({l, h[t][l]});
+}
+
+void tile_histograms(const Prepared& P, int64_t tw, int32_t T,
+                     std::vector<std::vector<std::pair<int64_t, int64_t>>>& hist) {
+    std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> out;
+    tile_histograms_multi(P, tw, std::vector<int32_t>{T}, out);
+    hist = std::move(out[0]);
 }
 
 spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L) {

@@ -91,6 +91,8 @@ int32_t paper_tile_count(const Prepared& P, int64_t tile_width);
 // hist[t] = vector of (length, count) pairs, lengths descending; zero rows go to the remainder.
 void tile_histograms(const Prepared& P, int64_t tile_width, int32_t num_tiles,
                      std::vector<std::vector<std::pair<int64_t, int64_t>>>& hist);
+void tile_histograms_multi(const Prepared& P, int64_t tile_width, const std::vector<int32_t>& num_tiles,
+                           std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>>& out);
 spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L);
 
 }  // namespace tc

@@ -281,10 +281,9 @@ static int x_mode(const Prepared& P, int32_t tw, int32_t T, int32_t t, bool cach
 }
 
 static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildParams& base, int32_t tw,
-                       int32_t T, const PerfTable& tab, bool stage = true) {
+                       int32_t T, const PerfTable& tab, bool stage,
+                       const std::vector<std::vector<std::pair<int64_t, int64_t>>>& hist) {
     Choice c{tw, T, {}, {}, 0.0};
-    std::vector<std::vector<std::pair<int64_t, int64_t>>> hist;
-    tile_histograms(P, tw, T, hist);
     const bool valued = !P.pattern;
     for (int32_t t = 0; t <= T; ++t) {
         const bool cached = stage && t < T && opt.stage_x != 0;
@@ -340,9 +339,11 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
             for (int32_t T = 0; T <= Tp; T = (T < 4 ? T + 1 : T * 2)) Ts.push_back(T);
             if (Ts.back() != Tp) Ts.push_back(Tp);
         }
-        for (int32_t T : Ts) {
-            if (T > 63) continue;
-            Choice c = evaluate(P, opt, bp, tw, T, tab);
+        Ts.erase(std::remove_if(Ts.begin(), Ts.end(), [](int32_t T) { return T > 63; }), Ts.end());
+        std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> hists;
+        tile_histograms_multi(P, tw, Ts, hists);           // one pass over the entries per width
+        for (size_t j = 0; j < Ts.size(); ++j) {
+            Choice c = evaluate(P, opt, bp, tw, Ts[j], tab, true, hists[j]);
             if (c.total < best.total) best = c;
         }
         if (opt.num_tiles >= 0 && opt.tile_width > 0) break;
@@ -353,10 +354,14 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
         for (int32_t tw : {1 << 20, 1 << 21, 1 << 22, 1 << 23}) {
             if ((double)tw * 4.0 > tab.l2_budget_bytes) continue;
             const int64_t max_tiles = (P.n_cols + tw - 1) / tw;
-            for (int32_t T : {1, 2, 4}) {
-                if (opt.num_tiles >= 0 && T != opt.num_tiles) continue;
-                if (T >= max_tiles) continue;
-                Choice c = evaluate(P, opt, bp, tw, T, tab, false);
+            std::vector<int32_t> Ts;
+            for (int32_t T : {1, 2, 4})
+                if ((opt.num_tiles < 0 || T == opt.num_tiles) && T < max_tiles) Ts.push_back(T);
+            if (Ts.empty()) continue;
+            std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> hists;
+            tile_histograms_multi(P, tw, Ts, hists);
+            for (size_t j = 0; j < Ts.size(); ++j) {
+                Choice c = evaluate(P, opt, bp, tw, Ts[j], tab, false, hists[j]);
                 if (c.total < best.total) best = c;
             }
         }
