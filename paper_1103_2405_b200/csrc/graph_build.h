@@ -2,6 +2,9 @@
 // clean-up, transposes, symmetric relabelling by column length.
 #pragma once
 #include <algorithm>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <cstdint>
 #include <vector>
 
@@ -59,15 +62,41 @@ inline void relabel_csr(int64_t N, const std::vector<int64_t>& rp, const std::ve
 }
 
 // transpose of an n x n pattern CSR (row v lists sources u ascending)
+// Parallel without atomics: thread j owns the target rows [v_j, v_{j+1}) and scans every entry in
+// source order, so each output row lists its sources ascending (the serial order) -- T read passes
+// over col instead of contended atomic counters on the hub rows.
 inline void transpose(int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
                       std::vector<int64_t>& trp, std::vector<int32_t>& tcol) {
     trp.assign(n + 1, 0);
-    for (int64_t k = 0; k < rp[n]; ++k) trp[col[k] + 1]++;
+    const int64_t m = rp[n];
+    int T = 1;
+#ifdef _OPENMP
+    T = std::max(1, omp_get_max_threads());
+#endif
+    if (m < (int64_t)1 << 20) T = 1;
+    std::vector<int64_t> vb(T + 1);
+    for (int j = 0; j <= T; ++j) vb[j] = n * j / T;
+    #pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int j = 0; j < T; ++j)
+        for (int64_t k = 0; k < m; ++k) {
+            const int32_t v = col[k];
+            if (v >= vb[j] && v < vb[j + 1]) trp[v + 1]++;
+        }
     for (int64_t i = 0; i < n; ++i) trp[i + 1] += trp[i];
-    tcol.resize(rp[n]);
+    // scatter ranges balanced by entry count
+    for (int j = 1; j < T; ++j)
+        vb[j] = std::upper_bound(trp.begin(), trp.end(), m * j / T) - trp.begin() - 1;
+    for (int j = 1; j <= T; ++j) vb[j] = std::max(vb[j], vb[j - 1]);
+    vb[T] = n;
+    tcol.resize(m);
     std::vector<int64_t> pos(trp.begin(), trp.end() - 1);
-    for (int64_t u = 0; u < n; ++u)
-        for (int64_t k = rp[u]; k < rp[u + 1]; ++k) tcol[pos[col[k]]++] = (int32_t)u;
+    #pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int j = 0; j < T; ++j)
+        for (int64_t u = 0; u < n; ++u)
+            for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+                const int32_t v = col[k];
+                if (v >= vb[j] && v < vb[j + 1]) tcol[pos[v]++] = (int32_t)u;
+            }
 }
 
 // Iteration matrix M of each algorithm in original vertex ids, and its column lengths:
