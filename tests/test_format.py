@@ -230,3 +230,16 @@ def test_plain_c_consumer(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
+
+
+def test_parallel_transpose_equals_serial(tmp_path):
+    """csrc/graph_build.h transpose (OpenMP, per-thread target ranges) is byte-equal to the serial
+    counting scatter, hub rows included."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "transpose_check")
+    r = subprocess.run(["g++", "-O2", "-fopenmp", "-std=c++17", "-I", os.path.join(root, "paper_1103_2405_b200", "csrc"),
+                        os.path.join(root, "tests", "c", "transpose_check.cpp"), "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
