@@ -355,7 +355,7 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
             if ((double)tw * 4.0 > tab.l2_budget_bytes) continue;
             const int64_t max_tiles = (P.n_cols + tw - 1) / tw;
             std::vector<int32_t> Ts;
-            for (int32_t T : {1, 2, 4})
+            for (int32_t T : {1, 2, 4})   // 6 / 8 / 12 measured equal on c4 (profiles/r01_c4_model.jsonl)
                 if ((opt.num_tiles < 0 || T == opt.num_tiles) && T < max_tiles) Ts.push_back(T);
             if (Ts.empty()) continue;
             std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> hists;
