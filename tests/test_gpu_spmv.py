@@ -218,3 +218,28 @@ def test_plain_c_consumer_on_gpu(gpu, tmp_path):
     p = np.fromfile(str(tmp_path / "p.bin"), np.float32).astype(np.float64)
     ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=k)
     assert np.abs(p - ref).sum() < 1e-6
+
+
+def test_host_batch_edge_cases(gpu):
+    """spmv_execute_host_batch: count 1, counts beyond the buffer depth, a rectangular matrix, the
+    error paths (negative count, null pointers with count > 0); every product equals the device
+    path bit for bit."""
+    import ctypes
+    import torch
+    from paper_1103_2405_b200 import Plan, _capi
+    rp, col, val = graphgen.random_csr(700, 1300, 20000, seed=9, kind="powerlaw", valued=True, signed=True)
+    p = Plan(700, 1300, rp, col, val, device=0, tile_width=256, num_tiles=2, workload_size=128)
+    for count in (1, 2, 7):
+        X = np.stack([graphgen.uniform_f32(1300, seed=50 + b, mode=2) for b in range(count)])
+        Y = p.execute_host_batch(X)
+        assert Y.shape == (count, 700)
+        for b in range(count):
+            y = torch.empty(700, device="cuda")
+            p.execute(torch.from_numpy(X[b]).cuda(), y)
+            torch.cuda.synchronize()
+            assert Y[b].tobytes() == y.cpu().numpy().tobytes()
+            check(Y[b], rp, col, val, X[b])
+    lib = _capi.lib()
+    assert lib.spmv_execute_host_batch(p._h, None, None, -1, None) != 0
+    assert lib.spmv_execute_host_batch(p._h, None, None, 3, None) != 0
+    assert lib.spmv_execute_host_batch(p._h, None, None, 0, None) == 0
