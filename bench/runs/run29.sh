@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-bash bench/run27.sh
+bash bench/runs/run27.sh
