@@ -123,7 +123,10 @@ spmv_status spmv_plan_create(int64_t n_rows, int64_t n_cols, int64_t nnz, const 
 void spmv_plan_destroy(spmv_plan plan);
 
 /* y = A x.  x_dev: n_cols floats in the caller's column order; y_dev: n_rows floats in the
- * caller's row order.  Asynchronous on `stream`.  Deterministic: bitwise identical across runs. */
+ * caller's row order.  Asynchronous on `stream`.  Deterministic: bitwise identical across runs.
+ * The plan's device scratch serves one product at a time: a call on a different stream than the
+ * plan's previous product first waits (cudaStreamWaitEvent) for that product, so products of one
+ * plan never overlap; use one plan per stream for concurrent products. */
 spmv_status spmv_execute(spmv_plan plan, const float* x_dev, float* y_dev, void* stream);
 
 /* Same product with x already in relabelled column order (xp_dev[k] = x[perm[k]]), as the

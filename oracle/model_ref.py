@@ -4,6 +4,11 @@ performance model (Sec. 3.3, Appendix E), for exact comparison with the
   pm_paper      Alg. 3 PM(T, WL) / Eq. 1-5
   partition     Alg. 2 Partition(T)
   tile_count    Alg. 1 (tile loop, lines 4-8)
+  pm_packed     Alg. 3 / Eq. 1-5 over the B200 packing (packed_workloads, wave_time)
+  tile_time_us  pm_packed + the B200 per-launch terms (launch, staging, y RMW, tail R31)
+Pins (tests/test_oracle_pins.py): pm_paper by Eq. 1's anchor and a hand-traced total;
+pm_packed equal to pm_paper in paper mode up to the clipped slots, and by two hand-traced B200
+packings; tile_time_us by hand-computed terms.
 Readings: R20 (table entry = whole-GPU slots/s at shape (w,h); Size counts padded slots;
 P_i unweighted mean), R22 (strict <, smallest WL wins ties), R23 (sum over every realised wave),
 R21 paper mode (empty candidate set -> WL_low).
@@ -79,23 +84,15 @@ def _rup(a, b):
     return (a + b - 1) // b * b
 
 
-def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32, orient=0):
-    """B200 reading of Alg. 3 (DESIGN.md "Autotuner"): the same wave model (Eq. 1-5) charged over
-    the workloads the format actually builds (the packing of Solution 3 / format_ref with row
-    splitting, R21, and clipping, R13), each looked up at its padded shape.
-    hist: [(row length, count)] with lengths descending.  perf(kind, w, h) -> slots/s.
-    Returns seconds."""
+def packed_workloads(hist, WL, align=8, split=True, ell_h=32, orient=0):
+    """The workloads the B200 packing walk forms over a tile (Solution 3 P:L88 with Alg. 3's
+    partition lines 8-15, reading R12; row splitting R21; clipping of the last workload R13):
+    a list of (kind, padded w, padded h, padded slots).  hist: [(row length, count)], lengths
+    descending."""
     rows = []
     for length, count in hist:
         rows += [length] * count
-    waves = []                                   # per wave: [sum perf, sum size, count]
-    def add(kind, w, h, size):
-        if not waves or waves[-1][2] == max_act_warp:
-            waves.append([0.0, 0.0, 0])
-        wv = waves[-1]
-        wv[0] += perf(kind, max(w, 1), h)
-        wv[1] += size
-        wv[2] += 1
+    out = []
     i = 0
     while i < len(rows):
         w = rows[i]
@@ -104,17 +101,64 @@ def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32, orien
             c = 0
             while c * WL < w:
                 wp = _rup(min(WL, w - c * WL), align)
-                add("rm", wp, 1, wp)
+                out.append(("rm", wp, 1, wp))
                 c += 1
             i += 1
         elif ((w > 0) if orient == 1 else (False if orient == 2 else w >= hq)):
             h = min(hq, len(rows) - i)
             wp = _rup(w, align)
-            add("rm", wp, h, h * wp)
+            out.append(("rm", wp, h, h * wp))
             i += h
         else:
             take = min(_rup(hq, ell_h), len(rows) - i)
             hs = _rup(take, ell_h)
-            add("cm", w, hs, hs * w)
+            out.append(("cm", w, hs, hs * w))
             i += take
-    return sum(S / (P / c) for P, S, c in waves)
+    return out
+
+
+def wave_time(workloads, perf, max_act_warp):
+    """Eq. 1-5 over a workload sequence: consecutive groups of MAX_ACT_WARP workloads form the
+    waves (Alg. 3 line 11), t_i = Size_i / mean P_i (Eq. 3-5), summed over every realised wave
+    (Eq. 2, R23).  perf(kind, w, h) -> slots/s."""
+    total = 0.0
+    for s in range(0, len(workloads), max_act_warp):
+        wave = workloads[s:s + max_act_warp]
+        P = sum(perf(k, max(w, 1), h) for k, w, h, _ in wave)
+        S = sum(size for *_, size in wave)
+        total += S / (P / len(wave))
+    return total
+
+
+def pm_packed(hist, WL, perf, max_act_warp, align=8, split=True, ell_h=32, orient=0):
+    """B200 reading of Alg. 3 (DESIGN.md "Autotuner"): the same wave model (Eq. 1-5) charged over
+    the workloads the format actually builds (packed_workloads), each looked up at its padded
+    shape.  Returns seconds."""
+    return wave_time(packed_workloads(hist, WL, align, split, ell_h, orient), perf, max_act_warp)
+
+
+def tile_time_us(hist, WL, perf, max_act_warp, *, tile_index, tile_width, cached, launch_us,
+                 stage_GBps, rmw_GBps, tail_frac=0.0, sm_count=148, align=8, split=True, ell_h=32,
+                 orient=0):
+    """Per-tile predicted time in microseconds: pm_packed plus the B200 terms the paper's model
+    does not carry (P:L220 names them qualitatively; R31):
+      launch      launch_us per non-empty tile ("restart a kernel for each tile", P:L62);
+      staging     cached tiles copy their x segment into every SM: tile_width * 4 B * sm_count
+                  at stage_GBps;
+      y RMW       tiles after the first read and write 8 B per touched row at rmw_GBps (P:L220);
+      tail (R31)  tail_frac of one workload's duration under load, WL / (mean P / MAX_ACT_WARP).
+    An empty tile costs nothing."""
+    wls = packed_workloads(hist, WL, align, split, ell_h, orient)
+    rows = sum(c for _, c in hist)
+    if not rows:
+        return 0.0
+    sec = wave_time(wls, perf, max_act_warp)
+    if tail_frac and wls:
+        mean_perf = sum(perf(k, max(w, 1), h) for k, w, h, _ in wls) / len(wls)
+        sec += tail_frac * WL * max_act_warp / mean_perf
+    us = sec * 1e6 + launch_us
+    if cached:
+        us += tile_width * 4.0 * sm_count / (stage_GBps * 1e3)
+    if tile_index > 0:
+        us += rows * 8.0 / (rmw_GBps * 1e3)
+    return us

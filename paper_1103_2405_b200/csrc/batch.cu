@@ -314,12 +314,15 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         s->batch = B;
         B->N = s->N;
         spmv_status bs = build_batch_plan(s, B);
-        if (bs) return bs;
+        if (!bs && B->tiles.empty()) { set_error("internal: batch plan has no tiles"); bs = SPMV_EINVAL; }
+        // a failed build leaves nothing attached: the next call starts over
+        if (bs) { batch_destroy(s); return bs; }
     }
     spmv_plan_s* p = B->plan;
     if (!B->exec) {
         const size_t vec = (size_t)(s->N + 4) * kQP * sizeof(float);
-#define CKB(x) do { if ((e = (x)) != cudaSuccess) return cuda_status(e, #x); } while (0)
+        // any failure below releases the whole batch state (buffers, graph, plan)
+#define CKB(x) do { if ((e = (x)) != cudaSuccess) { spmv_status r_ = cuda_status(e, #x); batch_destroy(s); return r_; } } while (0)
         CKB(cudaMalloc(&B->R, vec));
         CKB(cudaMalloc(&B->Z[0], vec));
         CKB(cudaMalloc(&B->Z[1], vec));
@@ -334,6 +337,7 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         // device-side loop: WHILE node around two iterations (double-buffered input)
         cudaGraph_t g;
         CKB(cudaGraphCreate(&g, 0));
+        B->graph = g;
         cudaGraphConditionalHandle h;
         CKB(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
         cudaGraphNodeParams cp = {};
@@ -349,11 +353,9 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         cudaError_t e2 = enqueue_batch_iteration(s, B, 1, st, h);
         cudaGraph_t cap = nullptr;
         e = cudaStreamEndCapture(st, &cap);
-        if (e1) return cuda_status(e1, "capture");
-        if (e2) return cuda_status(e2, "capture");
-        if (e) return cuda_status(e, "cudaStreamEndCapture");
+        if (!e) e = e1 ? e1 : e2;
+        CKB(e);
         CKB(cudaGraphInstantiate(&B->exec, g, 0));
-        B->graph = g;
 #undef CKB
     }
     B->Q = Q;

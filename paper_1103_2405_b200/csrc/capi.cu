@@ -94,6 +94,7 @@ static void free_device(spmv_plan_s* p) {
     if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
     if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
     for (auto& ev : p->ev_pipe) if (ev) cudaEventDestroy(ev);
+    if (p->ev_scratch) cudaEventDestroy(p->ev_scratch);
     cudaSetDevice(cur);
 }
 
@@ -229,6 +230,21 @@ spmv_status plan_final_positions(spmv_plan_s* p, std::vector<uint32_t>& entries,
     return SPMV_OK;
 }
 
+// Serialise products that share the plan's scratch across streams: wait for the
+// previous product when it ran on another stream; record the end of this one.
+static cudaError_t scratch_acquire(spmv_plan_s* p, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    if (!p->ev_scratch && (e = cudaEventCreateWithFlags(&p->ev_scratch, cudaEventDisableTiming))) return e;
+    if (p->scratch_used && p->scratch_stream != st) e = cudaStreamWaitEvent(st, p->ev_scratch, 0);
+    return e;
+}
+static cudaError_t scratch_release(spmv_plan_s* p, cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(p->ev_scratch, st);
+    p->scratch_stream = st;
+    p->scratch_used = true;
+    return e;
+}
+
 spmv_status execute_permuted(spmv_plan_s* p, const float* xp, float* y, cudaStream_t st) {
     return cuda_status(launch_tiles(*p, p->grid_tile, xp, EpiStore{y}, st), "tile launch");
 }
@@ -274,7 +290,11 @@ spmv_status spmv_execute_permuted(spmv_plan p, const float* xp, float* y, void* 
     if (p->device < 0) { set_error("host-only plan cannot execute"); return SPMV_EINVAL; }
     cudaError_t e = cudaSetDevice(p->device);
     if (e) return cuda_status(e, "cudaSetDevice");
-    return execute_permuted(p, xp, y, (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((e = scratch_acquire(p, st))) return cuda_status(e, "scratch order");
+    spmv_status s = execute_permuted(p, xp, y, st);
+    if ((e = scratch_release(p, st)) && !s) s = cuda_status(e, "scratch order");
+    return s;
 }
 
 __attribute__((visibility("default")))
@@ -284,10 +304,12 @@ spmv_status spmv_execute(spmv_plan p, const float* x, float* y, void* stream) {
     cudaError_t e = cudaSetDevice(p->device);
     if (e) return cuda_status(e, "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
-    if (p->n_cols > 0) {
-        if ((e = launch_permute(p, x, st))) return cuda_status(e, "permute_x");
-    }
-    return execute_permuted(p, p->d_xp, y, st);
+    if ((e = scratch_acquire(p, st))) return cuda_status(e, "scratch order");
+    spmv_status s = SPMV_OK;
+    if (p->n_cols > 0 && (e = launch_permute(p, x, st))) s = cuda_status(e, "permute_x");
+    if (!s) s = execute_permuted(p, p->d_xp, y, st);
+    if ((e = scratch_release(p, st)) && !s) s = cuda_status(e, "scratch order");
+    return s;
 }
 
 __attribute__((visibility("default")))
@@ -370,6 +392,7 @@ spmv_status spmv_execute_timed(spmv_plan p, const float* x, float* y, void* stre
     cudaError_t e = cudaSetDevice(p->device);
     if (e) return cuda_status(e, "cudaSetDevice");
     cudaStream_t st = (cudaStream_t)stream;
+    if ((e = scratch_acquire(p, st))) return cuda_status(e, "scratch order");
     std::vector<cudaEvent_t> ev;
     auto mark = [&]() { cudaEvent_t v; cudaEventCreate(&v); cudaEventRecord(v, st); ev.push_back(v); };
     mark();
@@ -382,6 +405,7 @@ spmv_status spmv_execute_timed(spmv_plan p, const float* x, float* y, void* stre
         if ((e = launch_tile(*p, t, p->grid_tile[t], p->d_xp, EpiStore{y}, st))) break;
         mark();
     }
+    if (!e) e = scratch_release(p, st);
     if (!e) e = cudaStreamSynchronize(st);
     for (size_t i = 1; i < ev.size(); ++i) {
         float ms = 0.f;

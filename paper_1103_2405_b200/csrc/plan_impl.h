@@ -50,6 +50,11 @@ struct spmv_plan_s {
     int32_t l1_hot_cols = 0;               // see TileArgs::hot; 0 = plain ld.global.nc (TCSPMV_L1_HOT)
     int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
+    // plan-owned scratch (d_xp, split partials and counters, claim queues) is used by one
+    // product at a time: a product on another stream than the previous one waits for it
+    cudaEvent_t ev_scratch = nullptr;
+    cudaStream_t scratch_stream = nullptr;
+    bool scratch_used = false;
 };
 
 namespace tc {

@@ -78,8 +78,13 @@ def test_random_bit_exact(seed):
     maxT = (nc + tw - 1) // tw
     T = int(rng.integers(0, min(maxT, 5) + 1))
     wls = [int(rng.integers(1, 300)) for _ in range(T + 1)]
+    split = seed % 5 != 0
+    if not split:
+        # paper mode (reading R21): WL at least the longest row of every tile
+        longest = int(np.diff(rp).max()) if nr else 1
+        wls = [max(w, longest, 1) for w in wls]
     ref, p = build_both(nr, nc, rp, col, val, tw, T, wls, align=[4, 8, 32][seed % 3],
-                        split=seed % 5 != 0 or True, camping=seed % 4 == 2)
+                        split=split, camping=seed % 4 == 2)
     assert_same(ref, p)
     r, c, v = p.to_coo()
     got = sorted(zip(r.tolist(), c.tolist(), v.tolist()))

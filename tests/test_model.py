@@ -43,40 +43,11 @@ def tile_hists(n_rows, n_cols, rp, col, tw, T):
 
 
 def expected_us(h, WL, t, T, tw, cached, split=True, tail_frac=0.0, orient=0):
-    sec = model_ref.pm_packed(h, WL, lambda k, w, hh: PERF[k], TABLE["max_act_warp"], split=split, orient=orient)
-    rows = sum(c for _, c in h)
-    if tail_frac and rows:
-        # reading R31: tail_frac of one workload's duration at the mean per-warp rate
-        kinds = workload_kinds(h, WL, orient=orient)
-        mean_perf = sum(PERF[k] for k in kinds) / len(kinds)
-        sec += tail_frac * WL * TABLE["max_act_warp"] / mean_perf
-    us = sec * 1e6
-    if rows:
-        us += TABLE["launch_us"]
-        if cached:
-            us += tw * 4.0 * 148 / (TABLE["stage_GBps"] * 1e3)
-        if t > 0:
-            us += rows * 8.0 / (TABLE["rmw_GBps"] * 1e3)
-    return us
-
-
-def workload_kinds(h, WL, ell_h=32, orient=0):
-    """Kinds of the workloads the packing walk forms (brute force over the expanded rows)."""
-    rows = [length for length, count in h for _ in range(count)]
-    kinds, i = [], 0
-    while i < len(rows):
-        w = rows[i]
-        hq = max(1, WL // max(w, 1))
-        if w > WL:
-            kinds += ["rm"] * (-(-w // WL))
-            i += 1
-        elif (w > 0) if orient == 1 else (orient == 0 and w >= hq):
-            kinds.append("rm")
-            i += min(hq, len(rows) - i)
-        else:
-            kinds.append("cm")
-            i += min(-(-hq // ell_h) * ell_h, len(rows) - i)
-    return kinds
+    # the oracle's per-tile prediction (pinned by hand in tests/test_oracle_pins.py)
+    return model_ref.tile_time_us(h, WL, lambda k, w, hh: PERF[k], TABLE["max_act_warp"], tile_index=t,
+                                  tile_width=tw, cached=cached, launch_us=TABLE["launch_us"],
+                                  stage_GBps=TABLE["stage_GBps"], rmw_GBps=TABLE["rmw_GBps"],
+                                  tail_frac=tail_frac, split=split, orient=orient)
 
 
 @pytest.mark.parametrize("seed,tail,orient", [(0, 0.0, 0), (1, 0.0, 0), (2, 0.0, 0), (3, 0.0, 0), (4, 0.5, 0),
@@ -162,13 +133,8 @@ def test_x_regime_per_tile(stage, budget, tmp_path):
         cached = bool(stage) and t < T
         mode = 1 if cached else (3 if span * 4.0 > budget else (2 if t == 0 else 0))
         prm, pcm = PERF_MODE[mode]
-        sec = model_ref.pm_packed(hists[t], wl, lambda k, w, h: prm if k == "rm" else pcm, TABLE["max_act_warp"])
-        rows = sum(c for _, c in hists[t])
-        us = sec * 1e6
-        if rows:
-            us += TABLE["launch_us"]
-            if cached:
-                us += tw * 4.0 * 148 / (TABLE["stage_GBps"] * 1e3)
-            if t > 0:
-                us += rows * 8.0 / (TABLE["rmw_GBps"] * 1e3)
+        us = model_ref.tile_time_us(hists[t], wl, lambda k, w, h: prm if k == "rm" else pcm,
+                                    TABLE["max_act_warp"], tile_index=t, tile_width=tw, cached=cached,
+                                    launch_us=TABLE["launch_us"], stage_GBps=TABLE["stage_GBps"],
+                                    rmw_GBps=TABLE["rmw_GBps"])
         assert math.isclose(st["tile_predicted_us"][t], us, rel_tol=1e-9), (t, mode, st["tile_predicted_us"][t], us)

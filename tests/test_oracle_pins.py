@@ -425,3 +425,115 @@ def test_alg2_candidate_set_hand_trace():
     # one PM call per candidate; for uniform rows of 100, h = WL // 100 = 1..5 (before padding)
     assert {h for _, h in seen} == {1, 2, 3, 4, 5}
     assert tried == [1, 2, 3, 4, 5]
+
+
+# --- pm_packed (the B200 reading of Alg. 3) pinned to the paper's pm_paper and by hand ---------
+def _hist(rows):
+    out = {}
+    for r in rows:
+        out[r] = out.get(r, 0) + 1
+    return sorted(out.items(), key=lambda kv: -kv[0])
+
+
+def _paper_sizes(rows, WL):
+    """Alg. 3 lines 7-15 written out again as a plain list of padded (w, h) shapes."""
+    i, out = 0, []
+    while i < len(rows):
+        w = rows[i]
+        h = WL // w
+        wp, hp = model_ref.padding(w, h)
+        out.append((wp, hp))
+        i += hp
+    return out
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("fill", [False, True])
+def test_pm_packed_equals_pm_paper_in_paper_mode(seed, fill):
+    """Paper mode (no split, align 32, WL >= longest row): the B200 walk forms the paper's
+    workloads.  The only difference is the last workload, which Alg. 3 counts at its
+    full padded shape and the format clips to the rows left (reading R13): equal when it is not
+    clipped, and with a uniform table the totals differ by exactly the clipped slots."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(5, 400))
+    rows = sorted((int(v) for v in rng.zipf(1.7, n) if v < 500), reverse=True) or [1]
+    WL = int(rows[0] * rng.integers(1, 4))
+    M = int(rng.integers(1, 50))
+    if fill:
+        # append rows of the last length until the paper's last workload is full (not clipped)
+        wp, hp = _paper_sizes(rows, WL)[-1]
+        used = sum(h for _, h in _paper_sizes(rows, WL)[:-1])
+        rows = rows + [rows[-1]] * (used + hp - len(rows))
+    shape_perf = lambda w, h: 1e9 * (1.0 + (w % 7) + 0.5 * (h % 5))   # any shape-dependent table
+    paper, _ = model_ref.pm_paper(rows, WL, shape_perf, M)
+    packed = model_ref.pm_packed(_hist(rows), WL, lambda k, w, h: shape_perf(w, h), M, align=32, split=False)
+    shapes = _paper_sizes(rows, WL)
+    wls = model_ref.packed_workloads(_hist(rows), WL, align=32, split=False)
+    assert len(wls) == len(shapes)
+    # all but the last workload agree shape by shape
+    assert [(w, h) for _, w, h, _ in wls[:-1]] == shapes[:-1]
+    clipped = sum(w * h for w, h in shapes) - sum(size for *_, size in wls)
+    assert clipped >= 0 and (clipped == 0) == fill
+    if clipped == 0:
+        assert math.isclose(packed, paper, rel_tol=1e-12)
+    up, _ = model_ref.pm_paper(rows, WL, lambda w, h: 1e9, M)
+    uk = model_ref.pm_packed(_hist(rows), WL, lambda k, w, h: 1e9, M, align=32, split=False)
+    assert math.isclose(up - uk, clipped / 1e9, rel_tol=1e-9, abs_tol=1e-18)
+
+
+def test_pm_packed_clipped_last_slab_hand_trace():
+    """Rows [4]*5 + [1]*40, WL 64.  Paper mode: 4 -> h = 16 -> column major, padded (4, 32);
+    1 -> h = 64, (1, 64): 128 + 64 = 192 slots.  The format clips the second slab to the 13 rows
+    left, padded to 32: 128 + 32 = 160 slots, 32 fewer."""
+    rows = [4] * 5 + [1] * 40
+    assert model_ref.pm_paper(rows, 64, lambda w, h: 1.0, 960)[0] == 192
+    wls = model_ref.packed_workloads(_hist(rows), 64, align=32, split=False)
+    assert wls == [("cm", 4, 32, 128), ("cm", 1, 32, 32)]
+    # MAX_ACT_WARP 1: one wave per workload, t = Size / P (Eq. 3 with P_i of one warp)
+    t = model_ref.pm_packed(_hist(rows), 64, lambda k, w, h: 2e9 if (w, h) == (4, 32) else 1e9, 1,
+                            align=32, split=False)
+    assert math.isclose(t, 128 / 2e9 + 32 / 1e9, rel_tol=1e-15)
+
+
+def test_pm_packed_split_row_hand_trace():
+    """Rows [70, 9, 9, 3, 2, 2, 1], WL 32, align 8, split (reading R21):
+      70 > WL -> chunks 32, 32, 6 -> RM (32,1), (32,1), (8,1);
+      9: hq = 3 <= 9 -> RM of 3 rows {9, 9, 3}, width 16 -> 48 slots;
+      2: hq = 16 > 2 -> CM, take min(32, 3 rows left) -> slab (2, 32) = 64 slots.
+    Sizes 32 + 32 + 8 + 48 + 64 = 184."""
+    h = _hist([70, 9, 9, 3, 2, 2, 1])
+    wls = model_ref.packed_workloads(h, 32, align=8, split=True)
+    assert wls == [("rm", 32, 1, 32), ("rm", 32, 1, 32), ("rm", 8, 1, 8), ("rm", 16, 3, 48), ("cm", 2, 32, 64)]
+    # uniform table: total = padded slots / throughput (SPEC.md L324)
+    assert math.isclose(model_ref.pm_packed(h, 32, lambda k, w, hh: 1e9, 2), 184e-9, rel_tol=1e-15)
+    # two-valued table, MAX_ACT_WARP 2: waves {32,32} rm, {8,48} rm, {64} cm at 4e9:
+    #   64/1e9 + 56/1e9 + 64/4e9 = 136e-9
+    two = lambda k, w, hh: 1e9 if k == "rm" else 4e9
+    assert math.isclose(model_ref.pm_packed(h, 32, two, 2), 136e-9, rel_tol=1e-15)
+    # MAX_ACT_WARP 3: waves {32,32,8} rm -> 72/1e9; {48 rm, 64 cm} -> mean P 2.5e9 -> 112/2.5e9
+    assert math.isclose(model_ref.pm_packed(h, 32, two, 3), 72e-9 + 44.8e-9, rel_tol=1e-15)
+
+
+def test_tile_time_us_terms_by_hand():
+    """The B200 per-launch terms, computed by hand.  Tile 2 of a tiling (y RMW charged), staged
+    (cached), 1000 rows of length 1, WL 100: w = 1 < hq = 100 -> column major, take =
+    min(rup(100, 32) = 128, rows left): 7 slabs of 128 rows and one of the last 104 rows (padded
+    to 128) = 8 workloads of 128 slots."""
+    h = [(1, 1000)]
+    wls = model_ref.packed_workloads(h, 100)
+    assert len(wls) == 8 and all(w == ("cm", 1, 128, 128) for w in wls[:7]) and wls[7] == ("cm", 1, 128, 128)
+    # 1000 = 7*128 + 104: the 8th slab takes the last 104 rows (padded to 128): 8 workloads
+    us = model_ref.tile_time_us(h, 100, lambda k, w, hh: 1e9, 4, tile_index=2, tile_width=65536, cached=True,
+                                launch_us=3.0, stage_GBps=5000.0, rmw_GBps=2500.0, tail_frac=0.5, sm_count=148)
+    waves = 8 * 128 / 1e9 * 1e6                                  # 1.024 us (uniform table)
+    tail = 0.5 * 100 * 4 / 1e9 * 1e6                             # 0.2 us
+    stage = 65536 * 4 * 148 / 5e6                                # 7.759462... us
+    rmw = 1000 * 8 / 2.5e6                                       # 3.2 us
+    assert math.isclose(us, waves + tail + 3.0 + stage + rmw, rel_tol=1e-12)
+    assert math.isclose(stage, 7.7594624, rel_tol=1e-9)
+    # first tile, unstaged: no staging, no RMW; an empty tile costs nothing
+    us0 = model_ref.tile_time_us(h, 100, lambda k, w, hh: 1e9, 4, tile_index=0, tile_width=65536, cached=False,
+                                 launch_us=3.0, stage_GBps=5000.0, rmw_GBps=2500.0)
+    assert math.isclose(us0, waves + 3.0, rel_tol=1e-12)
+    assert model_ref.tile_time_us([], 100, lambda k, w, hh: 1e9, 4, tile_index=1, tile_width=8, cached=True,
+                                  launch_us=3.0, stage_GBps=1.0, rmw_GBps=1.0) == 0.0
