@@ -55,7 +55,8 @@ typedef struct spmv_solver_s* spmv_solver;
 /* Options of the format builder (Sec. 3.1) and of the auto-tuner (Sec. 3.3).
  * spmv_options_default() fills: tile_width 0 (auto), num_tiles -1 (auto), workload_size -1
  * (auto), workload_sizes NULL, align_rm 8, split_long_rows 1, camping_pad 0, pattern 0,
- * ell_h 32, stage_x 1, perf_table_path NULL, orient 0. */
+ * ell_h 32, stage_x 1, perf_table_path NULL, orient 0, two_phase -1, pb_region / pb_chunk /
+ * pb_xcap / pb_group 0 (defaults). */
 typedef struct {
     int32_t tile_width;      /* columns per dense tile (paper: 64K, L60); 0 = chosen by the tuner */
     int32_t num_tiles;       /* dense tiles before the remainder; -1 = auto (Alg. 1 + B200 model);
@@ -75,6 +76,17 @@ typedef struct {
                                 single-format cases): 0 = composite (Alg. 3: row major iff
                                 w >= h), 1 = row major only (CSR-vector), 2 = column major only (ELL).
                                 Rows of length 0 and split chunks are unaffected. */
+    int32_t two_phase;       /* execution of the tiles: -1 = chosen by the performance
+                                model (default), 0 = one-pass tiles (x gathered through L1/L2),
+                                1 = two-phase tiles: every column tile's x segment is staged in
+                                shared memory (Solution 1, L56-L60) and its products are written
+                                to per-row-bin regions, which a second phase sums row by row with
+                                the composite split (Solution 3, L88) */
+    int32_t pb_region;       /* two-phase: products per row-bin region (0 = 8192; 32..65535) */
+    int32_t pb_chunk;        /* two-phase: entries per column chunk (0 = 8192) */
+    int32_t pb_xcap;         /* two-phase: columns per chunk x segment (0 = 8192; <= 65536) */
+    int64_t pb_group;        /* two-phase: products per group of bins kept L2-resident between the
+                                phases (0 = chosen from the L2 size) */
 } spmv_options;
 
 void spmv_options_default(spmv_options* opt);
@@ -97,6 +109,11 @@ typedef struct {
     int32_t composite_threshold[64]; /* first row length stored column major in each tile */
     int32_t resident_warps;     /* warps of one persistent tile launch (MAX_ACT_WARP of Eq. 1) */
     int32_t perf_table_loaded;  /* 1: measured offline table (Sec. 3.3), 0: built-in estimate */
+    int32_t two_phase;          /* 1: the plan executes as two-phase tiles (spmv_options.two_phase) */
+    int32_t pb_groups;          /* two-phase: groups, chunks, bins, long-row bins */
+    int64_t pb_chunks, pb_bins, pb_long_bins;
+    double one_pass_predicted_us;  /* model estimate of the one-pass tiles (Alg. 3 / Eq. 2) */
+    double two_phase_predicted_us; /* model estimate of the two-phase tiles */
 } spmv_plan_stats_t;
 
 /* Host view of the layout arrays (Format v1), valid while the plan lives, when the
@@ -165,6 +182,11 @@ spmv_status spmv_plan_layout(spmv_plan plan, spmv_layout_view* out);
 spmv_status spmv_plan_export(spmv_plan plan, const char* path);
 /* Decode the layout back to COO (original row / column ids), padding dropped; arrays of nnz. */
 spmv_status spmv_plan_to_coo(spmv_plan plan, int32_t* rows, int32_t* cols, float* vals);
+/* Diagnostic (two-phase plans): one product with a per-item timeline.  trace_host receives
+ * n_items x {SM id, start ns, reduce ready ns (0 for chunks), end ns} in work-queue order
+ * (globaltimer).  Synchronises.  Errors: EINVAL (not a device two-phase plan, buffer too small). */
+spmv_status spmv_pb_trace(spmv_plan plan, const float* x_dev, float* y_dev, void* stream,
+                          int64_t* trace_host, int64_t n_items);
 /* Number of kernel launches one spmv_execute issues (x permutation included). */
 int32_t spmv_plan_launches(spmv_plan plan);
 

@@ -22,7 +22,8 @@ class Options(ctypes.Structure):
                 ("workload_sizes", ctypes.POINTER(c_i32)), ("align_rm", c_i32),
                 ("split_long_rows", c_i32), ("camping_pad", c_i32), ("pattern", c_i32),
                 ("ell_h", c_i32), ("stage_x", c_i32), ("perf_table_path", ctypes.c_char_p),
-                ("orient", c_i32)]
+                ("orient", c_i32), ("two_phase", c_i32), ("pb_region", c_i32), ("pb_chunk", c_i32),
+                ("pb_xcap", c_i32), ("pb_group", c_i64)]
 
 
 class PlanStats(ctypes.Structure):
@@ -34,7 +35,9 @@ class PlanStats(ctypes.Structure):
                 ("tile_col_lo", c_i64 * 64), ("tile_col_hi", c_i64 * 64),
                 ("tile_staged", c_i32 * 64), ("tile_predicted_us", c_f64 * 64),
                 ("composite_threshold", c_i32 * 64), ("resident_warps", c_i32),
-                ("perf_table_loaded", c_i32)]
+                ("perf_table_loaded", c_i32), ("two_phase", c_i32), ("pb_groups", c_i32),
+                ("pb_chunks", c_i64), ("pb_bins", c_i64), ("pb_long_bins", c_i64),
+                ("one_pass_predicted_us", c_f64), ("two_phase_predicted_us", c_f64)]
 
 
 class LayoutView(ctypes.Structure):
@@ -76,6 +79,7 @@ SIGNATURES = {
     "spmv_plan_export": (c_i32, [c_vp, ctypes.c_char_p]),
     "spmv_needed_lists": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "spmv_plan_launches": (c_i32, [c_vp]),
+    "spmv_pb_trace": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64]),
     "spmv_iter_opts_default": (None, [ctypes.POINTER(IterOpts), ctypes.c_int]),
     "spmv_solver_create_local": (c_i32, [ctypes.c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                          ctypes.POINTER(IterOpts), ctypes.POINTER(Options), c_vp,

@@ -73,7 +73,11 @@ def _stats_dict(s: C.PlanStats) -> dict:
                 tile_staged=list(s.tile_staged[:T]),
                 tile_predicted_us=list(s.tile_predicted_us[:T]),
                 composite_threshold=list(s.composite_threshold[:T]),
-                resident_warps=s.resident_warps, perf_table_loaded=bool(s.perf_table_loaded))
+                resident_warps=s.resident_warps, perf_table_loaded=bool(s.perf_table_loaded),
+                two_phase=bool(s.two_phase), pb_groups=s.pb_groups, pb_chunks=s.pb_chunks,
+                pb_bins=s.pb_bins, pb_long_bins=s.pb_long_bins,
+                one_pass_predicted_us=s.one_pass_predicted_us,
+                two_phase_predicted_us=s.two_phase_predicted_us)
 
 
 class Plan:

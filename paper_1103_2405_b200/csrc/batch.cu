@@ -261,6 +261,7 @@ static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
     opt.tile_width = (int32_t)std::min<int64_t>(tw, INT32_MAX);
     opt.num_tiles = T;
     opt.stage_x = 0;
+    opt.two_phase = 0;         // the SpMM kernel runs on the one-pass tile layout
     if (opt.workload_size <= 0) opt.workload_size = p->opt.workload_size > 0 ? p->opt.workload_size : 1024;
     st = create_plan(p->n_rows, p->n_cols, p->nnz, rp.data(), col.data(), nullptr, &opt, s->device, &B->plan);
     if (st) return st;

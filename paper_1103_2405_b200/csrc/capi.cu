@@ -9,6 +9,7 @@
 #include <string>
 
 #include "launch.cuh"
+#include "pb_launch.cuh"
 #include "tune.h"
 
 namespace tc {
@@ -91,6 +92,9 @@ static void free_device(spmv_plan_s* p) {
     cudaFree(p->d_desc); cudaFree(p->d_row_id); cudaFree(p->d_col); cudaFree(p->d_val);
     cudaFree(p->d_perm); cudaFree(p->d_inv); cudaFree(p->d_xp); cudaFree(p->d_split); cudaFree(p->d_partials);
     cudaFree(p->d_counters); cudaFree(p->d_hx); cudaFree(p->d_sched); cudaFree(p->d_hxb);
+    cudaFree(p->d_pb_runs); cudaFree(p->d_pb_cd);
+    cudaFree(p->d_pb_val); cudaFree(p->d_pb_pos); cudaFree(p->d_pb_pmeta); cudaFree(p->d_pb_items);
+    cudaFree(p->d_pb_gchunks); cudaFree(p->d_pb_buf); cudaFree(p->d_pb_ctl);
     if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
     if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
     for (auto& ev : p->ev_pipe) if (ev) cudaEventDestroy(ev);
@@ -105,6 +109,85 @@ static cudaError_t build_stream_tables(spmv_plan_s* p) {
     p->stage_slots = (int32_t)std::max<int64_t>(64, (maxspan + 3) / 4 * 4);
     p->stream_grid = p->sm_count;
     return cudaSuccess;
+}
+
+// the device work queue: descriptors in queue order
+static std::vector<PbItem> pb_queue(const PbLayout& B) {
+    std::vector<PbItem> q(B.items.size());
+    for (size_t i = 0; i < B.items.size(); ++i) {
+        PbItem& t = q[i];
+        const int32_t code = B.items[i];
+        if (code >= 0) {
+            const PbChunk& c = B.chunks[code];
+            t.a0 = c.e0; t.a1 = c.gbase; t.a2 = c.run0; t.n = c.n; t.b0 = c.col0; t.b1 = c.span; t.b2 = c.nrun;
+            t.group = c.group; t.kind = PB_ITEM_EXPAND;
+        } else {
+            const PbBin& b = B.bins[~code];
+            t.a0 = b.roff; t.a1 = b.poff; t.a2 = b.row0; t.n = b.rlen; t.b0 = b.plen; t.b1 = b.nrows; t.b2 = b.nheavy;
+            t.group = b.group; t.kind = b.kind == PB_LONG ? PB_ITEM_LONG : PB_ITEM_BIN;
+        }
+    }
+    if (q.empty()) q.push_back(PbItem{});
+    return q;
+}
+
+// Two-phase plan (pb.h): layout over the original row and column ids (no relabel of x: the chunks
+// stage whatever columns they cover), uploaded with its partial buffer and queue counters.
+static spmv_status create_two_phase(spmv_plan_s* p, const Prepared& P, const int64_t* row_ptr,
+                                    const int32_t* col, const float* val, const PbParams& prm,
+                                    std::chrono::steady_clock::time_point t0) {
+    if (!pb_build(p->n_rows, p->n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, p->PB)) {
+        delete p; return SPMV_EINVAL;
+    }
+    PbLayout& B = p->PB;
+    p->perm.resize(p->n_cols);
+    for (int64_t k = 0; k < p->n_cols; ++k) p->perm[k] = (int32_t)k;
+    (void)P;
+    p->num_tiles = 0; p->tile_width = (int32_t)std::min<int64_t>(p->n_cols, INT32_MAX);
+    p->tiles.assign(1, TileInfo{});
+    p->tiles[0].col_hi = p->n_cols; p->tiles[0].nnz = p->nnz; p->tiles[0].rows = p->n_rows;
+    p->tiles[0].pred_us = p->two_phase_us;
+    p->predicted_us = p->two_phase_us;
+    p->n_row_entries = p->n_rows;
+    p->pb_chunks = (int64_t)B.chunks.size(); p->pb_bins = (int64_t)B.bins.size(); p->pb_groups = B.n_groups;
+    for (auto& b : B.bins) p->pb_long += b.kind == PB_LONG;
+    p->pb_smem = kPbStages * B.stage_bytes;
+    if (p->pb_smem > 227 * 1024) { delete p; set_error("two-phase stage exceeds shared memory"); return SPMV_EINVAL; }
+    p->L.row_id = B.prow;
+    p->host_valid = true;
+    p->pb_host_valid = true;
+    if (p->device >= 0) {
+        cudaError_t e;
+        int64_t& b = p->device_bytes;
+        std::vector<float> zbuf;
+        std::vector<uint32_t> zctl(2 + std::max(B.n_groups, 1), 0u);
+        // streams copied in 16-byte granules from a 16-byte boundary: 4 elements of tail padding
+        for (int i = 0; i < 4; ++i) {
+            B.runs.push_back(0); B.cd.push_back(0u); B.prow.push_back(PAD_ROW); B.pmeta.push_back(0u);
+            if (!p->pattern) B.val.push_back(0.0f);
+        }
+        if ((e = upload(&p->d_pb_runs, B.runs, b)) || (e = upload(&p->d_pb_cd, B.cd, b)) ||
+            (!p->pattern && (e = upload(&p->d_pb_val, B.val, b))) || (e = upload(&p->d_pb_pos, B.pos, b)) ||
+            (e = upload(&p->d_row_id, B.prow, b)) || (e = upload(&p->d_pb_pmeta, B.pmeta, b)) ||
+            (e = upload(&p->d_pb_items, pb_queue(B), b)) || (e = upload(&p->d_pb_gchunks, B.group_chunks, b)) ||
+            (e = upload(&p->d_pb_ctl, zctl, b))) {
+            free_device(p); delete p; return cuda_status(e, "two-phase upload");
+        }
+        if ((e = cudaMalloc(&p->d_pb_buf, (size_t)B.buf_floats * sizeof(float)))) {
+            free_device(p); delete p; return cuda_status(e, "two-phase buffer");
+        }
+        b += B.buf_floats * (int64_t)sizeof(float);
+        std::vector<float> xpz(p->n_cols + 4, 0.0f);
+        if ((e = upload(&p->d_xp, xpz, b))) { free_device(p); delete p; return cuda_status(e, "plan upload"); }
+        if ((e = pb_setup<EpiStore>(*p, p->pb_grid))) { free_device(p); delete p; return cuda_status(e, "occupancy"); }
+        // the per-entry arrays live on the device (fetched back on demand by to_coo)
+        B.cd = {}; B.val = {}; B.pos = {}; B.prow = {}; B.pmeta = {}; B.runs = {};
+        p->L.row_id = {};
+        p->host_valid = false;
+        p->pb_host_valid = false;
+    }
+    p->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return SPMV_OK;
 }
 
 // build the plan (host) and upload it; shared by spmv_plan_create and the solvers
@@ -135,10 +218,26 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     int32_t table_loaded = 0;
     st = choose_params(P, opt, sm_count, bp, pred, &table_loaded);
     if (st) return st;
+    if (opt.two_phase < -1 || opt.two_phase > 1) { set_error("two_phase must be -1, 0 or 1"); return SPMV_EINVAL; }
     spmv_plan_s* p = new spmv_plan_s();
     p->n_rows = n_rows; p->n_cols = n_cols; p->nnz = nnz; p->pattern = opt.pattern != 0;
     p->device = device; p->opt = opt; p->sm_count = sm_count; p->perf_table_loaded = table_loaded;
     p->opt.workload_sizes = nullptr; p->opt.perf_table_path = nullptr;
+    // one-pass tiles (Alg. 1-3) or two-phase tiles: the model's choice unless forced
+    const PbParams prm = pb_params(opt, n_cols, nnz);
+    for (double u : pred) p->one_pass_us += u;
+    p->two_phase_us = pb_predict_us(opt, n_rows, n_cols, nnz, opt.pattern == 0, prm);
+    // in auto mode an explicit one-pass parameter (tile width / count, WL, orientation, paper mode)
+    // asks for the one-pass tiles
+    const bool one_pass_forced = opt.tile_width > 0 || opt.num_tiles >= 0 || opt.workload_size > 0 ||
+                                 opt.workload_sizes || opt.orient != 0 || opt.split_long_rows == 0;
+    p->two_phase = opt.two_phase == 1 ||
+                   (opt.two_phase == -1 && !one_pass_forced && nnz > 0 && p->two_phase_us < p->one_pass_us);
+    if (p->two_phase) {
+        st = create_two_phase(p, P, row_ptr, col, val, prm, t0);
+        if (!st) *out = p;
+        return st;
+    }
     st = pack_layout(P, bp, p->L);
     if (st) { delete p; return st; }
     p->perm = std::move(P.perm);
@@ -211,6 +310,72 @@ static spmv_status ensure_host(spmv_plan_s* p) {
     return SPMV_OK;
 }
 
+// two-phase layout arrays back on the host (released after upload)
+static spmv_status pb_ensure_host(spmv_plan_s* p) {
+    if (p->pb_host_valid) return SPMV_OK;
+    cudaSetDevice(p->device);
+    PbLayout& B = p->PB;
+    int64_t nruns = 0, npos = 0;
+    for (auto& c : B.chunks) nruns = std::max<int64_t>(nruns, c.run0 + c.nrun);
+    for (auto& b : B.bins) npos = std::max<int64_t>(npos, b.poff + b.plen);
+    cudaError_t e;
+    if ((e = download(B.cd, p->d_pb_cd, p->nnz)) || (e = download(B.pos, p->d_pb_pos, npos)) ||
+        (e = download(B.prow, p->d_row_id, p->n_rows)) || (e = download(B.pmeta, p->d_pb_pmeta, p->n_rows)) ||
+        (e = download(B.runs, p->d_pb_runs, std::max<int64_t>(nruns, 1))) ||
+        (!p->pattern && (e = download(B.val, p->d_pb_val, p->nnz))))
+        return cuda_status(e, "two-phase layout download");
+    p->pb_host_valid = true;
+    return SPMV_OK;
+}
+
+// Decode the two-phase layout to COO: the expand's destination of every entry, then the reduce's
+// positions of every row (checks that every entry lands in exactly one row's list).
+static spmv_status pb_to_coo(spmv_plan_s* p, int32_t* rows, int32_t* cols, float* vals) {
+    spmv_status s = pb_ensure_host(p);
+    if (s) return s;
+    const PbLayout& B = p->PB;
+    std::vector<int64_t> src(B.buf_floats, -1);
+    std::vector<int32_t> ecol(p->nnz);
+    for (const PbChunk& c : B.chunks)
+        for (int32_t k = 0; k < c.n; ++k) {
+            const int64_t e = c.e0 + k;
+            const uint32_t w = B.cd[e];
+            const int64_t idx = c.gbase + k + B.runs[c.run0 + (w >> 16)];
+            if (idx < 0 || idx >= B.buf_floats || src[idx] >= 0) { set_error("two-phase destinations overlap"); return SPMV_EINVAL; }
+            src[idx] = e;
+            ecol[e] = c.col0 + (int32_t)(w & 0xffffu);
+        }
+    int64_t out = 0;
+    std::vector<uint8_t> seen(p->nnz, 0);
+    auto put = [&](uint32_t ent, int64_t idx) -> bool {
+        const int64_t e = idx >= 0 && idx < B.buf_floats ? src[idx] : -1;
+        if (e < 0 || seen[e] || out >= p->nnz) return false;
+        seen[e] = 1;
+        rows[out] = (int32_t)(ent & ROW_MASK);
+        cols[out] = ecol[e];
+        if (vals) vals[out] = p->pattern ? 1.0f : B.val[e];
+        ++out;
+        return true;
+    };
+    for (const PbBin& b : B.bins) {
+        if (b.kind == PB_LONG) {
+            for (int32_t q = 0; q < b.rlen; ++q)
+                if (!put(B.prow[b.row0], b.roff + q)) { set_error("two-phase decode"); return SPMV_EINVAL; }
+            continue;
+        }
+        for (int32_t r = 0; r < b.nrows; ++r) {
+            const uint32_t m = B.pmeta[b.row0 + r];
+            const int64_t po = m & 0xffffu, ln = m >> 16, stride = r < b.nheavy ? 1 : 32;
+            for (int64_t t = 0; t < ln; ++t)
+                if (!put(B.prow[b.row0 + r], b.roff + B.pos[b.poff + po + stride * t])) {
+                    set_error("two-phase decode"); return SPMV_EINVAL;
+                }
+        }
+    }
+    if (out != p->nnz) { set_error("two-phase decode count mismatch"); return SPMV_EINVAL; }
+    return SPMV_OK;
+}
+
 // Row-entry bookkeeping for entry-ordered epilogue state: the row entries (host copy) and, per
 // row, the index of its FINAL entry (the first one for split rows); -1 for rows without one.
 spmv_status plan_final_positions(spmv_plan_s* p, std::vector<uint32_t>& entries, std::vector<int32_t>& fpos) {
@@ -245,7 +410,21 @@ static cudaError_t scratch_release(spmv_plan_s* p, cudaStream_t st) {
     return e;
 }
 
+// the bulk copies of x segments need a 16-byte aligned x (else a copy in the plan's buffer)
+static const float* pb_x(spmv_plan_s* p, const float* x, cudaStream_t st, cudaError_t& e) {
+    e = cudaSuccess;
+    if (!(reinterpret_cast<uintptr_t>(x) & 15)) return x;
+    e = cudaMemcpyAsync(p->d_xp, x, p->n_cols * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    return p->d_xp;
+}
+
 spmv_status execute_permuted(spmv_plan_s* p, const float* xp, float* y, cudaStream_t st) {
+    if (p->two_phase) {
+        cudaError_t e;
+        xp = pb_x(p, xp, st, e);
+        if (e) return cuda_status(e, "x alignment copy");
+        return cuda_status(launch_pb(*p, p->pb_grid, xp, EpiStore{y}, st), "two-phase launch");
+    }
     return cuda_status(launch_tiles(*p, p->grid_tile, xp, EpiStore{y}, st), "tile launch");
 }
 
@@ -261,6 +440,7 @@ __attribute__((visibility("default"))) void spmv_options_default(spmv_options* o
     o->tile_width = 0; o->num_tiles = -1; o->workload_size = -1; o->workload_sizes = nullptr;
     o->align_rm = 8; o->split_long_rows = 1; o->camping_pad = 0; o->pattern = 0; o->ell_h = 32;
     o->stage_x = 1; o->perf_table_path = nullptr; o->orient = 0;
+    o->two_phase = -1; o->pb_region = 0; o->pb_chunk = 0; o->pb_xcap = 0; o->pb_group = 0;
 }
 
 __attribute__((visibility("default")))
@@ -306,8 +486,11 @@ spmv_status spmv_execute(spmv_plan p, const float* x, float* y, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if ((e = scratch_acquire(p, st))) return cuda_status(e, "scratch order");
     spmv_status s = SPMV_OK;
-    if (p->n_cols > 0 && (e = launch_permute(p, x, st))) s = cuda_status(e, "permute_x");
-    if (!s) s = execute_permuted(p, p->d_xp, y, st);
+    if (p->two_phase) s = execute_permuted(p, x, y, st);    // no relabel of x (pb.h)
+    else {
+        if (p->n_cols > 0 && (e = launch_permute(p, x, st))) s = cuda_status(e, "permute_x");
+        if (!s) s = execute_permuted(p, p->d_xp, y, st);
+    }
     if ((e = scratch_release(p, st)) && !s) s = cuda_status(e, "scratch order");
     return s;
 }
@@ -396,11 +579,15 @@ spmv_status spmv_execute_timed(spmv_plan p, const float* x, float* y, void* stre
     std::vector<cudaEvent_t> ev;
     auto mark = [&]() { cudaEvent_t v; cudaEventCreate(&v); cudaEventRecord(v, st); ev.push_back(v); };
     mark();
-    if (p->n_cols > 0) {
+    if (p->two_phase) {
+        const float* xa = pb_x(p, x, st, e);
+        if (!e) e = launch_pb(*p, p->pb_grid, xa, EpiStore{y}, st);
+        mark();
+    } else if (p->n_cols > 0) {
         launch_permute(p, x, st);
         mark();
     }
-    for (int32_t t = 0; t <= p->num_tiles; ++t) {
+    for (int32_t t = 0; t <= p->num_tiles && !p->two_phase; ++t) {
         if (p->tiles[t].wl_end == p->tiles[t].wl_begin) continue;
         if ((e = launch_tile(*p, t, p->grid_tile[t], p->d_xp, EpiStore{y}, st))) break;
         mark();
@@ -417,8 +604,32 @@ spmv_status spmv_execute_timed(spmv_plan p, const float* x, float* y, void* stre
 }
 
 __attribute__((visibility("default")))
+spmv_status spmv_pb_trace(spmv_plan p, const float* x, float* y, void* stream, int64_t* trace_host,
+                          int64_t n_items) {
+    if (!p || !x || !y || !trace_host) { set_error("null argument"); return SPMV_EINVAL; }
+    if (!p->two_phase || p->device < 0) { set_error("not a device two-phase plan"); return SPMV_EINVAL; }
+    const int64_t ni = (int64_t)p->PB.items.size();
+    if (n_items < ni) { set_error("trace buffer too small"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t* d = nullptr;
+    if ((e = cudaMalloc(&d, std::max<int64_t>(ni, 1) * 4 * sizeof(int64_t)))) return cuda_status(e, "trace");
+    cudaMemsetAsync(d, 0, std::max<int64_t>(ni, 1) * 4 * sizeof(int64_t), st);
+    const float* xa = pb_x(p, x, st, e);
+    if (e || (e = scratch_acquire(p, st)) || (e = launch_pb(*p, p->pb_grid, xa, EpiStore{y}, st, d)) ||
+        (e = scratch_release(p, st)) || (e = cudaStreamSynchronize(st)) ||
+        (e = cudaMemcpy(trace_host, d, ni * 4 * sizeof(int64_t), cudaMemcpyDeviceToHost))) {
+        cudaFree(d); return cuda_status(e, "trace run");
+    }
+    cudaFree(d);
+    return SPMV_OK;
+}
+
+__attribute__((visibility("default")))
 int32_t spmv_plan_launches(spmv_plan p) {
     if (!p) return 0;
+    if (p->two_phase) return 1;
     int32_t n = p->n_cols > 0 ? 1 : 0;
     for (auto& t : p->tiles) n += (t.wl_end > t.wl_begin) ? 1 : 0;
     return n;
@@ -441,12 +652,17 @@ spmv_status spmv_plan_stats(spmv_plan p, spmv_plan_stats_t* o) {
     }
     o->resident_warps = p->grid_tile.empty() ? 0 : p->grid_tile.back() * (p->stream ? kStreamThreads / 32 : kWarps);
     o->perf_table_loaded = p->perf_table_loaded;
+    o->two_phase = p->two_phase ? 1 : 0;
+    o->pb_groups = p->pb_groups; o->pb_chunks = p->pb_chunks; o->pb_bins = p->pb_bins; o->pb_long_bins = p->pb_long;
+    o->one_pass_predicted_us = p->one_pass_us; o->two_phase_predicted_us = p->two_phase_us;
+    if (p->two_phase) o->resident_warps = p->pb_grid * kPbWarps;
     return SPMV_OK;
 }
 
 __attribute__((visibility("default")))
 spmv_status spmv_plan_layout(spmv_plan p, spmv_layout_view* v) {
     if (!p || !v) { set_error("null argument"); return SPMV_EINVAL; }
+    if (p->two_phase) { set_error("two-phase plan: no one-pass tile layout (use spmv_plan_to_coo)"); return SPMV_EINVAL; }
     spmv_status s = ensure_host(p);
     if (s) return s;
     HostLayout& L = p->L;
@@ -504,6 +720,7 @@ spmv_status spmv_plan_export(spmv_plan p, const char* path) {
 __attribute__((visibility("default")))
 spmv_status spmv_plan_to_coo(spmv_plan p, int32_t* rows, int32_t* cols, float* vals) {
     if (!p || (p->nnz > 0 && (!rows || !cols))) { set_error("null argument"); return SPMV_EINVAL; }
+    if (p->two_phase) return pb_to_coo(p, rows, cols, vals);
     spmv_status s = ensure_host(p);
     if (s) return s;
     const HostLayout& L = p->L;

@@ -495,6 +495,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         spmv_options opt;
         if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
         opt.pattern = 1;
+        opt.two_phase = 0;     // the row-partitioned epilogue runs on the one-pass tiles
         if ((st = tc::create_plan(D->n_local, n, lrp[D->n_local], lrp.data(), lcol.data(), nullptr, &opt, device, &s->plan))) throw st;
         spmv_plan_s* p = s->plan;
         // the plan's columns are ordered by local length: the first nzc have entries

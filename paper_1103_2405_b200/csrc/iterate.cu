@@ -26,6 +26,7 @@
 #include "epilogues.cuh"
 #include "graph_build.h"
 #include "launch.cuh"
+#include "pb_launch.cuh"
 #include "solver.h"
 
 namespace tc {
@@ -87,13 +88,18 @@ static spmv_status build_solver(spmv_solver_s* s, const int64_t* row_ptr, const 
     CKE(cudaMalloc(&s->d_ctrl, sizeof(Ctrl)));
     CKE(cudaMemset(s->d_ctrl, 0, sizeof(Ctrl)));
     // launches and partial slots
-    if (s->algo == SPMV_ALGO_HITS) CKE(setup_grids<EpiHitsSpmv>(*p, s->grids));
+    if (p->two_phase) {             // one persistent two-phase launch per SpMV (pb.h)
+        int g = 0;
+        if (s->algo == SPMV_ALGO_HITS) CKE(pb_setup<EpiHitsSpmv>(*p, g));
+        else CKE(pb_setup<EpiAffine>(*p, g));
+        s->grids.assign(1, g);
+    } else if (s->algo == SPMV_ALGO_HITS) CKE(setup_grids<EpiHitsSpmv>(*p, s->grids));
     else CKE(setup_grids<EpiAffine>(*p, s->grids));
     s->tiles_used.clear();
     s->slot_base.clear();
     int32_t slots = 0;
     for (int32_t t = 0; t <= p->num_tiles; ++t) {
-        if (p->tiles[t].wl_end == p->tiles[t].wl_begin) continue;
+        if (!p->two_phase && p->tiles[t].wl_end == p->tiles[t].wl_begin) continue;
         s->tiles_used.push_back(t);
         s->slot_base.push_back(slots);
         slots += s->grids[t];
@@ -136,7 +142,8 @@ static cudaError_t enqueue_iteration(spmv_solver_s* s, int parity, cudaStream_t 
             epi.y = s->d_y; epi.half = s->d_half_e; epi.fpos = s->d_fpos; epi.ctrl = s->d_ctrl; epi.slots = s->d_slots;
             epi.slot_base = s->slot_base[i]; epi.total_slots = s->total_slots;
             epi.is_last = (i + 1 == nu); epi.l2 = s->it.hits_norm != 1;
-            cudaError_t e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], s->d_p, epi, st);
+            cudaError_t e = p->two_phase ? launch_pb(*p, s->grids[0], s->d_p, epi, st)
+                                         : launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], s->d_p, epi, st);
             if (e) return e;
         }
         hits_normalize<<<s->norm_grid, kThreads, 0, st>>>(s->d_y, s->d_p, s->d_half, s->N, s->d_ctrl,
@@ -150,7 +157,8 @@ static cudaError_t enqueue_iteration(spmv_solver_s* s, int parity, cudaStream_t 
         epi.ctrl = s->d_ctrl; epi.slots = s->d_slots; epi.slot_base = s->slot_base[i];
         epi.total_slots = s->total_slots; epi.is_last = (i + 1 == nu); epi.cond = cond;
         epi.rwr = s->algo == SPMV_ALGO_RWR;
-        cudaError_t e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], s->d_z[parity], epi, st);
+        cudaError_t e = p->two_phase ? launch_pb(*p, s->grids[0], s->d_z[parity], epi, st)
+                                     : launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], s->d_z[parity], epi, st);
         if (e) return e;
     }
     return cudaSuccess;

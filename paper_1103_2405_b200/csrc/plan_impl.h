@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "pb.h"
 #include "plan.h"
 
 struct spmv_plan_s {
@@ -50,6 +51,25 @@ struct spmv_plan_s {
     int32_t l1_hot_cols = 0;               // see TileArgs::hot; 0 = plain ld.global.nc (TCSPMV_L1_HOT)
     int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
+    // two-phase tiles (pb.h): when set, the plan has no one-pass tiles; d_row_id holds the
+    // two-phase row order (row | FLAG_FINAL, n_row_entries = n_rows) for the epilogues
+    bool two_phase = false;
+    tc::PbLayout PB;                      // host copy; the per-entry arrays are released after upload
+    bool pb_host_valid = false;
+    int32_t* d_pb_runs = nullptr;
+    uint32_t* d_pb_cd = nullptr;
+    float* d_pb_val = nullptr;
+    uint16_t* d_pb_pos = nullptr;
+    uint32_t* d_pb_pmeta = nullptr;
+    tc::PbItem* d_pb_items = nullptr;
+    int32_t* d_pb_gchunks = nullptr;
+    float* d_pb_buf = nullptr;
+    uint32_t* d_pb_ctl = nullptr;
+    int64_t pb_smem = 0;
+    int pb_grid = 0;                      // persistent grid of the EpiStore instantiation
+    int64_t pb_chunks = 0, pb_bins = 0, pb_long = 0;
+    int32_t pb_groups = 0;
+    double one_pass_us = 0.0, two_phase_us = 0.0;
     // plan-owned scratch (d_xp, split partials and counters, claim queues) is used by one
     // product at a time: a product on another stream than the previous one waits for it
     cudaEvent_t ev_scratch = nullptr;

@@ -46,6 +46,10 @@ struct PerfTable {
     double rmw_GBps = 4000.0;       // y read-modify-write of accumulating rows
     double tail_frac = 0.0;         // launch tail: this fraction of one workload's duration under load
     double l2_budget_bytes = 96e6;  // x spans above this are served by DRAM (mode 3, reading R32)
+    // two-phase tiles: measured time per work item of one persistent CTA
+    double pb_item_us = 3.2;           // valued
+    double pb_item_us_pattern = 2.95;
+    double pb_launch_us = 4.0;
     int max_act_warp = 148 * 32;
     bool loaded = false;
     std::string source = "built-in";
@@ -109,6 +113,9 @@ static bool parse_table(const std::string& text, PerfTable& T) {
     if (num_after("tail_frac", v)) T.tail_frac = v;
     if (num_after("max_act_warp", v)) T.max_act_warp = (int)v;
     if (num_after("l2_budget_bytes", v)) T.l2_budget_bytes = v;
+    if (num_after("pb_item_us", v)) T.pb_item_us = v;
+    if (num_after("pb_item_us_pattern", v)) T.pb_item_us_pattern = v;
+    if (num_after("pb_launch_us", v)) T.pb_launch_us = v;
     size_t p = text.find("\"entries\"");
     if (p == std::string::npos) return false;
     p = text.find('[', p);
@@ -380,6 +387,50 @@ void predict_plan(spmv_plan_s& p, const std::vector<double>& pred_us) {
         p.tiles[t].pred_us = pred_us[t];
         p.predicted_us += pred_us[t];
     }
+}
+
+// ------------------------------------------------------------------ two-phase tiles (pb.h)
+// Group size: the live part of the partial buffer (about four groups: one being expanded, one
+// being reduced, the ones in between) stays in L2 beside x, capped at 8 M products (a larger group
+// holds more bins than a chunk's run table, so its chunks shrink; measured on c2 and c4,
+// DESIGN.md 7c).
+PbParams pb_params(const spmv_options& opt, int64_t n_cols, int64_t nnz) {
+    PbParams prm;
+    const PerfTable tab = table_for(opt.perf_table_path);
+    if (opt.pb_region > 0) prm.rcap = opt.pb_region;
+    if (opt.pb_chunk > 0) prm.ccap = opt.pb_chunk;
+    if (opt.pb_xcap > 0) prm.xcap = opt.pb_xcap;
+    prm.pcap = std::min<int32_t>(65535, std::max<int32_t>(1024, prm.rcap + prm.rcap / 2));
+    if (opt.pb_group > 0) prm.gcap = opt.pb_group;
+    else {
+        const double free_l2 = std::max(0.0, tab.l2_budget_bytes - 4.0 * (double)n_cols);
+        prm.gcap = std::min<int64_t>(8 << 20, std::max<int64_t>(1 << 20, (int64_t)(free_l2 / (4.0 * 4.0))));
+    }
+    (void)nnz;
+    return prm;
+}
+
+// Model of the two-phase tiles.  Both phases run out of shared-memory stages filled by bulk
+// copies, so time is set by how many items the persistent CTAs get through: t = items * t_item /
+// CTAs + launch, with t_item measured on B200 (a CTA's two-stage pipeline at two CTAs per SM:
+// 3.2 us per item valued, 2.95 us pattern; c2 valued 29.7 K items in 325 us, pattern 304 us; c4:
+// 1.05 M items in 13.7 ms).
+// The item count is estimated from the parameters: bins of ~rcap products, and chunks cut by
+// whichever of ccap entries, xcap columns or nrcap distinct bins binds first.
+double pb_predict_us(const spmv_options& opt, int64_t n_rows, int64_t n_cols, int64_t nnz, bool valued,
+                     const PbParams& prm) {
+    const PerfTable tab = table_for(opt.perf_table_path);
+    const double m = (double)nnz;
+    if (m <= 0) return tab.pb_launch_us;
+    const double groups = std::max(1.0, std::ceil(m / (double)prm.gcap));
+    const double bins = std::max(m / (0.8 * prm.rcap), (double)n_rows / prm.maxrows);
+    const double per_col = m / (groups * std::max<double>(1.0, (double)n_cols));   // entries per column per group
+    const double bins_g = bins / groups;
+    double e_chunk = std::min<double>(prm.ccap, std::max(1.0, prm.xcap * per_col));
+    if (bins_g > 2.0 * prm.nrcap) e_chunk = std::min<double>(e_chunk, prm.nrcap);
+    const double chunks = m / e_chunk;
+    const double ctas = 2.0 * 148.0;
+    return tab.pb_launch_us + (chunks + bins) * (valued ? tab.pb_item_us : tab.pb_item_us_pattern) / ctas;
 }
 
 }  // namespace tc

@@ -3,6 +3,7 @@
 #pragma once
 #include <vector>
 
+#include "pb.h"
 #include "plan.h"
 
 struct spmv_plan_s;
@@ -12,5 +13,9 @@ namespace tc {
 spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_count,
                           BuildParams& bp, std::vector<double>& pred_us, int32_t* table_loaded = nullptr);
 void predict_plan(spmv_plan_s& p, const std::vector<double>& pred_us);
+// two-phase tiles (pb.h): parameters from the options and the L2 budget, and the byte model
+PbParams pb_params(const spmv_options& opt, int64_t n_cols, int64_t nnz);
+double pb_predict_us(const spmv_options& opt, int64_t n_rows, int64_t n_cols, int64_t nnz, bool valued,
+                     const PbParams& prm);
 
 }  // namespace tc
