@@ -3,7 +3,8 @@
 
 Workload (BASELINE.json configs[1]): LiveJournal-shaped R-MAT graph,
 n = 4,847,571 vertices, m = 68,993,773 edges, valued (edge values U(0,1]), fp32.
-Step: one tiled-composite SpMV y = A x through spmv_execute (x permutation + every tile launch),
+Step: one tiled-composite SpMV y = A x through spmv_execute in the execution the performance model
+picks (two-phase tiles on c2: one persistent launch; one-pass tiles: x relabel + every tile launch),
 inputs resident in HBM.  Metric: SpMV GFLOP/s (= 2 m / step time); HBM GB/s and the PageRank /
 HITS / RWR iteration rates on the same graph are reported beside it.
 N > 1 (torchrun): every rank runs its own replica of the workload (independent problems, no
@@ -112,6 +113,27 @@ class ClockSampler:
                 continue
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measure_traffic(kernel):
+    """DRAM bytes (read + write) of the last captured launch of `kernel`, or None."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    try:
+        out = subprocess.run([ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "-k",
+                              f"regex:{kernel}", "-s", "2", "-c", "1", "--csv", sys.executable,
+                              os.path.join(ROOT, "bench", "ncu_traffic.py")],
+                             capture_output=True, text=True, timeout=300).stdout
+        tot, unit = 0.0, {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        import csv as _csv
+        for row in _csv.reader(l for l in out.splitlines() if l.startswith('"')):
+            if len(row) > 3 and row[-3].startswith("dram__bytes_"):
+                tot += float(row[-1].replace(",", "")) * unit.get(row[-2], 1)
+        return tot or None
+    except Exception:
+        return None
 
 
 def load_workload():
@@ -237,16 +259,23 @@ def main():
                                                       buf.ctypes.data, nl), "spmv_execute_timed")
         per += buf
     per /= reps
-    # launch 0 = x permutation (12 B per column), then the non-empty tiles in order
-    tiles = [t for t in range(st["num_tiles"] + 1) if st["tile_nnz"][t] > 0 or t == st["num_tiles"]]
-    launch_bytes = [12.0 * G.n]
-    launch_names = ["permute_x"]
-    launch_nnz = [0]
-    for t in tiles[: nl - 1]:
-        launch_nnz.append(st["tile_nnz"][t])
-        width = st["tile_col_hi"][t] - st["tile_col_lo"][t]
-        launch_bytes.append(8.0 * st["tile_nnz"][t] + 8.0 * st["tile_rows"][t] + 4.0 * width)
-        launch_names.append(f"tc_spmv_tile[{t}]" + ("(smem x)" if st["tile_staged"][t] else "(L1/L2 x)"))
+    if st["two_phase"]:
+        # two-phase tiles: one persistent launch, no x relabel; its algorithmic
+        # bytes are the whole product's (8 m + 12 n valued)
+        launch_bytes = [8.0 * G.m + 12.0 * G.n]
+        launch_names = ["pb_spmv(two-phase tiles)"]
+        launch_nnz = [G.m]
+    else:
+        # launch 0 = x permutation (12 B per column), then the non-empty tiles in order
+        tiles = [t for t in range(st["num_tiles"] + 1) if st["tile_nnz"][t] > 0 or t == st["num_tiles"]]
+        launch_bytes = [12.0 * G.n]
+        launch_names = ["permute_x"]
+        launch_nnz = [0]
+        for t in tiles[: nl - 1]:
+            launch_nnz.append(st["tile_nnz"][t])
+            width = st["tile_col_hi"][t] - st["tile_col_lo"][t]
+            launch_bytes.append(8.0 * st["tile_nnz"][t] + 8.0 * st["tile_rows"][t] + 4.0 * width)
+            launch_names.append(f"tc_spmv_tile[{t}]" + ("(smem x)" if st["tile_staged"][t] else "(L1/L2 x)"))
     dom = int(np.argmax(per))
     peak, peak_src = peaks()
     ach = launch_bytes[dom] / (per[dom] * 1e-3) / 1e9
@@ -272,16 +301,16 @@ def main():
                                   "probe": "profiles/r01_probe_gather.jsonl skew S=%d" % best["S"]}
     except Exception:
         pass
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(launch_names[dom].split("(")[0])
-            if tr:
-                roofline["traffic"] = tr
-                # effective DRAM bytes per stored entry vs the minimum 8 + 12 n / m
-                roofline["dram_bytes_per_nnz"] = round(tr / G.m, 2)
-                roofline["min_bytes_per_nnz"] = round(8 + 12 * G.n / G.m, 2)
-    except Exception:
-        pass
+    # DRAM traffic of the dominant kernel, measured in this run: one ncu pass (dram bytes only)
+    # over a fresh process that builds the same plan and launches it three times
+    if rank == 0 and world == 1 and not os.environ.get("TCSPMV_BENCH_NO_NCU"):
+        tr = measure_traffic("pb_spmv" if st["two_phase"] else "tc_spmv_tile")
+        if tr:
+            roofline["traffic"] = tr
+            roofline["traffic_source"] = "ncu dram__bytes_read.sum + dram__bytes_write.sum, this run (bench/ncu_traffic.py)"
+            # effective DRAM bytes per stored entry vs the minimum 8 + 12 n / m
+            roofline["dram_bytes_per_nnz"] = round(tr / G.m, 2)
+            roofline["min_bytes_per_nnz"] = round(8 + 12 * G.n / G.m, 2)
 
     # end to end through the public API with host buffers: spmv_execute_host_batch copies every
     # step's x in (pinned H2D) and its y out (D2H) inside the timed region, overlapping the copies
@@ -417,14 +446,16 @@ def main():
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "parallelism": f"replicas{world}",
                        "l2": "inputs larger than L2 (0.57 GB of col/val streamed per step); x (19 MB) L2-resident",
-                       "plan": {k: st[k] for k in ("num_tiles", "tile_width", "wl", "tile_staged",
-                                                     "n_workloads", "n_slots")}},
+                       "plan": {k: st[k] for k in ("two_phase", "num_tiles", "tile_width", "wl", "tile_staged",
+                                                     "n_workloads", "n_slots", "pb_groups", "pb_chunks",
+                                                     "pb_bins", "one_pass_predicted_us",
+                                                     "two_phase_predicted_us")}},
             "hbm_GBps_algorithmic": round(hbm_gbs, 1),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(args.steps * nl),
-            "clocks": clk.summary(t0, t1),
+            "clocks": clk.summary(t_soak, t1),
             "predicted_us": round(st["predicted_us"], 2),
             "plan_build_ms": round(st["build_ms"], 1),      # one-time, amortised, not in the step
             "batches_ms_per_step": {"n": nb, "median": round(float(np.median(batch_ms)), 5),

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "epilogues.cuh"
+#include "graph_build.h"
 #include "launch.cuh"
 #include "solver.h"
 
@@ -209,6 +210,11 @@ struct BatchState {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     std::vector<double> residual;
+    // the batch's vertex space: the solver's, or (two-phase solver plans, whose graph keeps its
+    // given order) relabelled by column length so the batch's one-pass tiles need no x permute
+    std::vector<int32_t> pi;            // original vertex -> batch row
+    float* inv = nullptr;               // 1/deg in batch order
+    bool own_inv = false;
 };
 
 static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int parity, int32_t slot_base,
@@ -220,7 +226,7 @@ static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int pari
     a.col = p->d_col; a.row_id = p->d_row_id; a.col_lo = ti.col_lo;
     a.width = (int32_t)(ti.col_hi - ti.col_lo);
     a.split = p->d_split; a.partials = B->partials; a.counters = p->d_counters;
-    a.Z = B->Z[parity]; a.Znext = B->Z[parity ^ 1]; a.R = B->R; a.Y = B->Y; a.inv = s->d_inv;
+    a.Z = B->Z[parity]; a.Znext = B->Z[parity ^ 1]; a.R = B->R; a.Y = B->Y; a.inv = B->inv;
     a.q = B->q; a.c = (float)s->it.c; a.ctrl = s->d_ctrl; a.slots = B->slots; a.res_out = B->res;
     a.slot_base = slot_base; a.total_slots = total_slots; a.is_last = is_last; a.cond = cond;
     return a;
@@ -256,6 +262,26 @@ static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
         for (int64_t k = 0; k < p->nnz; ++k) col[fill[rows[k]]++] = cols[k];
     }
     rows = {}; cols = {};
+    B->pi = s->pi;
+    B->inv = s->d_inv;
+    if (p->two_phase) {
+        // symmetric relabel by column length (Solution 2, L66), composed with the solver's order
+        std::vector<int64_t> clen(p->n_cols, 0);
+        for (int64_t k = 0; k < p->nnz; ++k) clen[col[k]]++;
+        std::vector<int32_t> sigma;
+        order_by_length(clen, sigma);
+        Coo R;
+        relabel_csr(p->n_rows, rp, col, sigma, R);
+        rp = std::move(R.rp); col = std::move(R.col);
+        for (auto& v : B->pi) v = sigma[v];
+        std::vector<float> inv(p->n_rows), inv_b(p->n_rows);
+        cudaError_t e = cudaMemcpy(inv.data(), s->d_inv, p->n_rows * sizeof(float), cudaMemcpyDeviceToHost);
+        if (e) return cuda_status(e, "batch inv");
+        for (int64_t i = 0; i < p->n_rows; ++i) inv_b[sigma[i]] = inv[i];
+        if ((e = cudaMalloc(&B->inv, std::max<int64_t>(p->n_rows, 1) * sizeof(float)))) { B->inv = nullptr; return cuda_status(e, "batch inv"); }
+        B->own_inv = true;
+        if ((e = cudaMemcpy(B->inv, inv_b.data(), p->n_rows * sizeof(float), cudaMemcpyHostToDevice))) return cuda_status(e, "batch inv");
+    }
     spmv_options opt = p->opt;
     opt.pattern = 1; opt.workload_sizes = nullptr; opt.perf_table_path = nullptr;
     opt.tile_width = (int32_t)std::min<int64_t>(tw, INT32_MAX);
@@ -361,14 +387,14 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
     }
     B->Q = Q;
     std::vector<int32_t> hq(kQP, -1);
-    for (int32_t i = 0; i < Q; ++i) hq[i] = s->pi[queries[i]];
+    for (int32_t i = 0; i < Q; ++i) hq[i] = B->pi[queries[i]];
     Ctrl c{};
     c.c = s->it.c; c.tol = s->it.tol; c.max_iter = s->it.max_iter; c.fixed_iters = s->it.fixed_iters;
     c.inv_n = 1.0 / (double)s->n; c.residual = INFINITY; c.q = -1;
     if ((e = cudaMemcpyAsync(B->q, hq.data(), kQP * sizeof(int32_t), cudaMemcpyHostToDevice, st)) ||
         (e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st)))
         return cuda_status(e, "upload");
-    spmm_init<<<p->sm_count * 8, 256, 0, st>>>(B->R, B->Z[0], s->d_inv, B->q, s->N);
+    spmm_init<<<p->sm_count * 8, 256, 0, st>>>(B->R, B->Z[0], B->inv, B->q, s->N);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
@@ -401,7 +427,7 @@ spmv_status spmv_solver_result_batch(spmv_solver s, float* out) {
     cudaError_t e = cudaMemcpy(R.data(), B->R, R.size() * sizeof(float), cudaMemcpyDeviceToHost);
     if (e) return cuda_status(e, "result");
     for (int32_t qi = 0; qi < B->Q; ++qi)
-        for (int64_t u = 0; u < s->n; ++u) out[(size_t)qi * s->n + u] = R[(size_t)s->pi[u] * kQP + qi];
+        for (int64_t u = 0; u < s->n; ++u) out[(size_t)qi * s->n + u] = R[(size_t)B->pi[u] * kQP + qi];
     return SPMV_OK;
 }
 
@@ -414,6 +440,7 @@ void batch_destroy(spmv_solver s) {
     if (B->graph) cudaGraphDestroy(B->graph);
     cudaFree(B->R); cudaFree(B->Z[0]); cudaFree(B->Z[1]); cudaFree(B->Y); cudaFree(B->partials);
     cudaFree(B->q); cudaFree(B->slots); cudaFree(B->res);
+    if (B->own_inv) cudaFree(B->inv);
     if (B->plan) spmv_plan_destroy(B->plan);
     delete B;
     s->batch = nullptr;

@@ -135,11 +135,12 @@ static std::vector<PbItem> pb_queue(const PbLayout& B) {
 // stage whatever columns they cover), uploaded with its partial buffer and queue counters.
 static spmv_status create_two_phase(spmv_plan_s* p, const Prepared& P, const int64_t* row_ptr,
                                     const int32_t* col, const float* val, const PbParams& prm,
-                                    std::chrono::steady_clock::time_point t0) {
-    if (!pb_build(p->n_rows, p->n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, p->PB)) {
+                                    std::chrono::steady_clock::time_point t0, bool built) {
+    if (!built && !pb_build(p->n_rows, p->n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, p->PB)) {
         delete p; return SPMV_EINVAL;
     }
     PbLayout& B = p->PB;
+    if (!built) p->two_phase_us = pb_predict_items_us(p->opt, (int64_t)B.items.size(), !p->pattern);
     p->perm.resize(p->n_cols);
     for (int64_t k = 0; k < p->n_cols; ++k) p->perm[k] = (int32_t)k;
     (void)P;
@@ -231,10 +232,19 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     // asks for the one-pass tiles
     const bool one_pass_forced = opt.tile_width > 0 || opt.num_tiles >= 0 || opt.workload_size > 0 ||
                                  opt.workload_sizes || opt.orient != 0 || opt.split_long_rows == 0;
-    p->two_phase = opt.two_phase == 1 ||
-                   (opt.two_phase == -1 && !one_pass_forced && nnz > 0 && p->two_phase_us < p->one_pass_us);
+    p->two_phase = opt.two_phase == 1;
+    bool built = false;
+    if (opt.two_phase == -1 && !one_pass_forced && nnz > 0 && p->two_phase_us < 1.25 * p->one_pass_us) {
+        // close enough to matter: build the layout and predict from its actual item count
+        if (pb_build(n_rows, n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, p->PB)) {
+            built = true;
+            p->two_phase_us = pb_predict_items_us(opt, (int64_t)p->PB.items.size(), !p->pattern);
+            p->two_phase = p->two_phase_us < p->one_pass_us;
+        }
+        if (!p->two_phase) p->PB = PbLayout();
+    }
     if (p->two_phase) {
-        st = create_two_phase(p, P, row_ptr, col, val, prm, t0);
+        st = create_two_phase(p, P, row_ptr, col, val, prm, t0, built);
         if (!st) *out = p;
         return st;
     }

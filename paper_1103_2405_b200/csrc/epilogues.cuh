@@ -107,6 +107,11 @@ struct EpiAffine {
         return q;
     }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
+    // two-phase tiles: the rows' p and 1/deg (entry order) into L2 ahead of the rows
+    __device__ __forceinline__ void prefetch_rows(int64_t e0, int32_t n, uint64_t pol) const {
+        prefetch_l2_range(p + e0, 4LL * n, pol);
+        prefetch_l2_range(inv_deg + e0, 4LL * n, pol);
+    }
     __device__ __forceinline__ void commit(uint32_t ent, int32_t e, float v, const Pre& pre) {
         const uint32_t r = ent & ROW_MASK;
         v += pre.acc;
@@ -165,6 +170,9 @@ struct EpiHitsSpmv {
         return q;
     }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
+    __device__ __forceinline__ void prefetch_rows(int64_t e0, int32_t n, uint64_t pol) const {
+        prefetch_l2_range(half + e0, n, pol);
+    }
     __device__ __forceinline__ void commit(uint32_t ent, int32_t, float v, const Pre& pre) {
         const uint32_t r = ent & ROW_MASK;
         v += pre.acc;

@@ -117,15 +117,27 @@ __device__ __forceinline__ PbItem load_item(const PbItem* p) {
     return r;
 }
 
+// broadcast a plain struct from lane `src` (word by word)
+template <class T>
+__device__ __forceinline__ T shfl_pod(const T& v, int src) {
+    static_assert(sizeof(T) % 4 == 0, "shuffled structs are whole 32-bit words");
+    T out;
+    const uint32_t* a = reinterpret_cast<const uint32_t*>(&v);
+    uint32_t* b = reinterpret_cast<uint32_t*>(&out);
+    #pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) b[i] = __shfl_sync(0xffffffffu, a[i], src);
+    return out;
+}
+
 // ------------------------------------------------------------------ producer (one thread)
 __device__ __forceinline__ void stage_copy(uint8_t* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                            uint64_t pol) {
     if (bytes) bulk_g2s(dst, src, bytes, bar, pol);
 }
 
-template <bool VALUED>
+template <bool VALUED, class Epi>
 __device__ __forceinline__ void produce(const PbArgs& a, int32_t it, const PbItem& t, uint8_t* stage,
-                                        uint64_t* full, uint64_t pol_stream, uint64_t pol_x) {
+                                        uint64_t* full, uint64_t pol_stream, uint64_t pol_x, const Epi& epi) {
     PbStage* h = reinterpret_cast<PbStage*>(stage);
     uint8_t* d = stage + 128;
     h->item = it;
@@ -182,6 +194,7 @@ __device__ __forceinline__ void produce(const PbArgs& a, int32_t it, const PbIte
         h->o_b = (int32_t)off; off += bpos;
         h->o_c = (int32_t)off; off += brow;
         h->o_d = (int32_t)off;
+        epi.prefetch_rows(row0, nrows, pol_stream);   // per-row epilogue state into L2
         mbar_arrive_expect_tx(full, breg + bpos + 2 * brow);
         stage_copy(d, a.buf + roff, breg, full, pol_stream);
         stage_copy(d + h->o_b, a.pos + poff, bpos, full, pol_stream);
@@ -263,31 +276,62 @@ __device__ __forceinline__ void consume_reduce(const PbArgs& a, const PbStage& h
     for (int i = tid; i < nlines; i += kPbConsumers) discard_l2_line(reg_g + 32 * i);
     const float* reg = reinterpret_cast<const float*>(d + h.o_a);
     const uint16_t* ps = reinterpret_cast<const uint16_t*>(d + h.o_b);
-    // heavy rows: warp per row (CSR-vector)
-    for (int r = warp; r < nheavy; r += kPbConsumerWarps) {
-        const uint32_t m = pmeta[r];
-        const int po = (int)(m & 0xffffu), ln = (int)(m >> 16);
-        float acc = 0.0f;
-        for (int k = lane; k < ln; k += 32) acc += reg[ps[po + k]];
-        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) epi.write(prow[r], (int32_t)(row0 + r), acc);
-    }
-    // light rows: thread per row over column-major 32-row slabs (ELL)
-    for (int li = tid; li < nrows - nheavy; li += kPbConsumers) {
-        const int r = nheavy + li;
-        const uint32_t ent = prow[r];
-        const typename Epi::Pre pre = epi.prefetch(ent, (int32_t)(row0 + r));
-        const uint32_t m = pmeta[r];
-        const int po = (int)(m & 0xffffu), ln = (int)(m >> 16);
-        float acc = 0.0f;
-        int k = 0;
-        for (; k + 4 <= ln; k += 4) {
-            const float v0 = reg[ps[po + 32 * k]], v1 = reg[ps[po + 32 * (k + 1)]];
-            const float v2 = reg[ps[po + 32 * (k + 2)]], v3 = reg[ps[po + 32 * (k + 3)]];
-            acc += v0; acc += v1; acc += v2; acc += v3;
+    // heavy rows: warp per row (CSR-vector).  The epilogue operands of the warp's next
+    // 32 heavy rows are requested at once, one row per lane, and handed to lane 0 by shuffles.
+    for (int r0 = warp; r0 < nheavy; r0 += 32 * kPbConsumerWarps) {
+        const int rl = r0 + lane * kPbConsumerWarps;
+        const uint32_t ent_l = rl < nheavy ? prow[rl] : PAD_ROW;
+#ifdef PB_EXP_NOPRE
+        const typename Epi::Pre pre_l{};
+#else
+        const typename Epi::Pre pre_l = epi.prefetch(ent_l, (int32_t)(row0 + rl));
+#endif
+        for (int j = 0; j < 32; ++j) {
+            const int r = r0 + j * kPbConsumerWarps;
+            if (r >= nheavy) break;
+            const uint32_t m = pmeta[r];
+            const int po = (int)(m & 0xffffu), ln = (int)(m >> 16);
+            float acc = 0.0f;
+            for (int k = lane; k < ln; k += 32) acc += reg[ps[po + k]];
+            for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const typename Epi::Pre pre = shfl_pod(pre_l, j);
+            if (lane == 0) epi.commit(prow[r], (int32_t)(row0 + r), acc, pre);
         }
-        for (; k < ln; ++k) acc += reg[ps[po + 32 * k]];
-        epi.commit(ent, (int32_t)(row0 + r), acc, pre);
+    }
+    // light rows: thread per row over column-major 32-row slabs (ELL); the epilogue
+    // operands of all of a thread's rows are requested before any of them is summed
+    constexpr int LR = 4;
+    const int nlight = nrows - nheavy;
+    for (int l0 = tid; l0 < nlight; l0 += LR * kPbConsumers) {
+        uint32_t ent[LR], m[LR];
+        typename Epi::Pre pre[LR];
+        #pragma unroll
+        for (int j = 0; j < LR; ++j) {
+            const int li = l0 + j * kPbConsumers;
+            const int r = nheavy + li;
+            ent[j] = li < nlight ? prow[r] : PAD_ROW;
+            m[j] = li < nlight ? pmeta[r] : 0u;
+#ifdef PB_EXP_NOPRE
+            pre[j] = typename Epi::Pre{};
+#else
+            pre[j] = epi.prefetch(ent[j], (int32_t)(row0 + r));
+#endif
+        }
+        #pragma unroll
+        for (int j = 0; j < LR; ++j) {
+            const int li = l0 + j * kPbConsumers;
+            if (li >= nlight) break;
+            const int po = (int)(m[j] & 0xffffu), ln = (int)(m[j] >> 16);
+            float acc = 0.0f;
+            int k = 0;
+            for (; k + 4 <= ln; k += 4) {
+                const float v0 = reg[ps[po + 32 * k]], v1 = reg[ps[po + 32 * (k + 1)]];
+                const float v2 = reg[ps[po + 32 * (k + 2)]], v3 = reg[ps[po + 32 * (k + 3)]];
+                acc += v0; acc += v1; acc += v2; acc += v3;
+            }
+            for (; k < ln; ++k) acc += reg[ps[po + 32 * k]];
+            epi.commit(ent[j], (int32_t)(row0 + nheavy + li), acc, pre[j]);
+        }
     }
 }
 
@@ -344,7 +388,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_spmv(PbArgs a, Epi epi_in) {
                         if (pend_g[q] >= 0 && pend_g[q] <= t.group) retire(q);
                 uint8_t* stage = pb_sm + (size_t)s * a.stage_bytes;
                 if (a.trace && it < a.n_items) a.trace[4 * (int64_t)it + 1] = gtimer();
-                produce<VALUED>(a, it, t, stage, &full[s], pol_stream, pol_x);
+                produce<VALUED>(a, it, t, stage, &full[s], pol_stream, pol_x, epi);
                 if (it >= a.n_items) break;
                 pend_k[s] = k;
                 pend_g[s] = t.kind == PB_ITEM_EXPAND ? t.group : -1;

@@ -68,6 +68,14 @@ __device__ __forceinline__ void bulk_prefetch_l2_hint(const void* src, uint32_t 
                  : "memory");
 }
 
+// [p, p + bytes) into L2 (any alignment: widened to 16-byte granules)
+__device__ __forceinline__ void prefetch_l2_range(const void* p, int64_t bytes, uint64_t pol) {
+    if (bytes <= 0) return;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + (uintptr_t)bytes + 15) & ~(uintptr_t)15;
+    bulk_prefetch_l2_hint(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo), pol);
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -647,6 +647,8 @@ struct EpiStore {
     }
     __device__ __forceinline__ void commit(uint32_t ent, int32_t, float v, const Pre& pre) { y[ent & ROW_MASK] = v + pre.acc; }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
+    // two-phase tiles: per-row state of entries [e0, e0 + n) into L2 ahead of the rows (none here)
+    __device__ __forceinline__ void prefetch_rows(int64_t, int32_t, uint64_t) const {}
 };
 
 }  // namespace tc

@@ -433,4 +433,10 @@ double pb_predict_us(const spmv_options& opt, int64_t n_rows, int64_t n_cols, in
     return tab.pb_launch_us + (chunks + bins) * (valued ? tab.pb_item_us : tab.pb_item_us_pattern) / ctas;
 }
 
+// the same model over a built layout's actual item count
+double pb_predict_items_us(const spmv_options& opt, int64_t items, bool valued) {
+    const PerfTable tab = table_for(opt.perf_table_path);
+    return tab.pb_launch_us + (double)items * (valued ? tab.pb_item_us : tab.pb_item_us_pattern) / (2.0 * 148.0);
+}
+
 }  // namespace tc

@@ -17,5 +17,6 @@ void predict_plan(spmv_plan_s& p, const std::vector<double>& pred_us);
 PbParams pb_params(const spmv_options& opt, int64_t n_cols, int64_t nnz);
 double pb_predict_us(const spmv_options& opt, int64_t n_rows, int64_t n_cols, int64_t nnz, bool valued,
                      const PbParams& prm);
+double pb_predict_items_us(const spmv_options& opt, int64_t items, bool valued);
 
 }  // namespace tc
