@@ -303,6 +303,13 @@ spmv_status spmv_needed_lists(int64_t n, const int64_t* row_ptr, const int32_t* 
 spmv_status spmv_comm_unique_id(void* id_out_128_bytes);
 spmv_status spmv_comm_create(int rank, int world, const void* nccl_unique_id, int device,
                              spmv_comm* out);
+/* Test transport: `world` logical ranks in one process on one `device`, written
+ * to out[0 .. world).  Each handle is driven by its own host thread (one rank each, as with NCCL);
+ * the per-iteration exchange, the needed-columns segments and the metadata allgather become
+ * device-to-device copies between the ranks' buffers behind the same interface, ordered by
+ * events and host barriers.  Lets the row-partitioned code path (slots, offsets, packing, rank-
+ * order partial sums) run and be checked on one GPU.  Destroy every handle.  Errors: EINVAL, ECUDA. */
+spmv_status spmv_comm_create_loopback(int world, int device, spmv_comm* out);
 void spmv_comm_destroy(spmv_comm comm);
 
 const char* spmv_last_error(void);

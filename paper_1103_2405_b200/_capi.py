@@ -103,6 +103,7 @@ SIGNATURES = {
     "spmv_partition_plan": (c_i32, [c_i64, c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(c_i64)]),
     "spmv_comm_unique_id": (c_i32, [c_vp]),
     "spmv_comm_create": (c_i32, [ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
+    "spmv_comm_create_loopback": (c_i32, [ctypes.c_int, ctypes.c_int, c_vp]),
     "spmv_comm_destroy": (None, [c_vp]),
     "spmv_last_error": (ctypes.c_char_p, []),
     "spmv_version": (ctypes.c_char_p, []),

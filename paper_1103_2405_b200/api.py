@@ -371,12 +371,23 @@ class Comm:
             dist.broadcast_object_list(obj, src=0, group=group)
         return cls(rank, world, obj[0], device)
 
-    def __init__(self, rank: int, world: int, uid: bytes, device: int):
-        buf = ctypes.create_string_buffer(bytes(uid), 128)
-        h = ctypes.c_void_p()
-        check(C.lib().spmv_comm_create(rank, world, buf, device, ctypes.byref(h)), "spmv_comm_create")
-        self._h = h
+    def __init__(self, rank: int, world: int, uid: bytes, device: int, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+        else:
+            buf = ctypes.create_string_buffer(bytes(uid), 128)
+            h = ctypes.c_void_p()
+            check(C.lib().spmv_comm_create(rank, world, buf, device, ctypes.byref(h)), "spmv_comm_create")
+            self._h = h
         self.rank, self.world = rank, world
+
+    @classmethod
+    def loopback(cls, world: int, device: int = 0):
+        """Test transport: `world` logical ranks on one device (spmv_comm_create_loopback); drive
+        each returned communicator from its own thread."""
+        arr = (ctypes.c_void_p * world)()
+        check(C.lib().spmv_comm_create_loopback(world, device, arr), "spmv_comm_create_loopback")
+        return [cls(r, world, b"", device, _handle=ctypes.c_void_p(arr[r])) for r in range(world)]
 
     def close(self):
         if getattr(self, "_h", None):

@@ -4,7 +4,10 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <numeric>
 #include <vector>
 
@@ -57,9 +60,35 @@ struct Nccl {
 Nccl g_nccl;
 }  // namespace
 
+// Loopback transport (test transport, spmv_comm_create_loopback): `world` logical ranks in one
+// process on one device, one host thread and stream each.  The same exchange() interface moves the
+// data with device-to-device copies: every rank publishes (buffer, event) at a host barrier, then
+// pulls the pieces it receives from its peers' buffers on its own stream, and a second barrier
+// (with the copies' events) keeps a peer from overwriting its slot before everyone has read it.
+namespace {
+struct Loopback {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long gen = 0;
+    std::vector<const void*> ptr;           // published buffer per rank
+    std::vector<const int64_t*> offs;       // published per-peer offsets (needed mode)
+    std::vector<cudaEvent_t> ready, done;   // per rank: data ready / copies out of it finished
+    std::vector<std::vector<char>> host;    // metadata allgather
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long g = gen;
+        if (++arrived == world) { arrived = 0; ++gen; cv.notify_all(); }
+        else cv.wait(lk, [&] { return gen != g; });
+    }
+};
+}  // namespace
+
 struct spmv_comm_s {
     int rank = 0, world = 1, device = 0;
     NcclComm comm = nullptr;
+    std::shared_ptr<Loopback> lb;           // loopback transport (no NCCL)
 };
 
 static spmv_status nccl_status(int r, const char* what) {
@@ -193,9 +222,41 @@ spmv_status spmv_comm_create(int rank, int world, const void* uid, int device, s
     return SPMV_OK;
 }
 
+__attribute__((visibility("default")))
+spmv_status spmv_comm_create_loopback(int world, int device, spmv_comm* out) {
+    if (!out || world < 1) { set_error("invalid argument"); return SPMV_EINVAL; }
+    cudaError_t e = cudaSetDevice(device);
+    if (e) return cuda_status(e, "cudaSetDevice");
+    auto lb = std::make_shared<Loopback>();
+    lb->world = world;
+    lb->ptr.assign(world, nullptr);
+    lb->offs.assign(world, nullptr);
+    lb->ready.assign(world, nullptr);
+    lb->done.assign(world, nullptr);
+    lb->host.assign(world, {});
+    for (int r = 0; r < world; ++r) {
+        if ((e = cudaEventCreateWithFlags(&lb->ready[r], cudaEventDisableTiming)) ||
+            (e = cudaEventCreateWithFlags(&lb->done[r], cudaEventDisableTiming))) {
+            for (auto ev : lb->ready) if (ev) cudaEventDestroy(ev);
+            for (auto ev : lb->done) if (ev) cudaEventDestroy(ev);
+            return cuda_status(e, "loopback events");
+        }
+    }
+    for (int r = 0; r < world; ++r) {
+        spmv_comm_s* c = new spmv_comm_s();
+        c->rank = r; c->world = world; c->device = device; c->lb = lb;
+        out[r] = c;
+    }
+    return SPMV_OK;
+}
+
 __attribute__((visibility("default"))) void spmv_comm_destroy(spmv_comm c) {
     if (!c) return;
     if (c->comm) g_nccl.CommDestroy(c->comm);
+    if (c->lb && c->lb.use_count() == 1) {
+        for (auto ev : c->lb->ready) if (ev) cudaEventDestroy(ev);
+        for (auto ev : c->lb->done) if (ev) cudaEventDestroy(ev);
+    }
     delete c;
 }
 
@@ -342,8 +403,35 @@ __global__ void fill_f(float* a, int64_t n, float v) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
 }
 
+// loopback: pull piece q of every peer q into `dst` (src_q + soff(q) -> dst + doff(q), n(q) floats)
+template <class Src, class Dst, class Cnt>
+spmv_status loopback_pull(spmv_comm c, const void* mine, const int64_t* my_offs, Src src_off, Dst dst_off, Cnt cnt,
+                          float* dst, cudaStream_t st) {
+    Loopback& L = *c->lb;
+    const int r = c->rank;
+    cudaError_t e = cudaEventRecord(L.ready[r], st);
+    L.ptr[r] = mine;
+    L.offs[r] = my_offs;
+    L.barrier();                                        // every peer's data is enqueued
+    for (int q = 0; q < c->world && !e; ++q) {
+        if (q == r || cnt(q) == 0) continue;
+        if (!(e = cudaStreamWaitEvent(st, L.ready[q], 0)))
+            e = cudaMemcpyAsync(dst + dst_off(q), static_cast<const float*>(L.ptr[q]) + src_off(q, L.offs[q]),
+                                (size_t)cnt(q) * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    }
+    if (!e) e = cudaEventRecord(L.done[r], st);
+    L.barrier();                                        // every copy out of our buffer is enqueued
+    for (int q = 0; q < c->world && !e; ++q)
+        if (q != r) e = cudaStreamWaitEvent(st, L.done[q], 0);
+    L.barrier();                                        // events free for the next round
+    return cuda_status(e, "loopback exchange");
+}
+
 spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
     if (c->world == 1) return SPMV_OK;
+    if (c->lb)
+        return loopback_pull(c, G, nullptr, [&](int q, const int64_t*) { return (int64_t)q * slot; },
+                             [&](int q) { return (int64_t)q * slot; }, [&](int) { return slot; }, G, st);
     return nccl_status(g_nccl.AllGather(G + (int64_t)c->rank * slot, G, (size_t)slot, ncclFloat32, c->comm, st),
                        "ncclAllGather");
 }
@@ -354,6 +442,12 @@ spmv_status exchange(spmv_comm c, Dist* D, const tc::Ctrl* ctrl, int sm_count, c
     if (!D->exchange) return allgather(c, D->d_G, D->slot, st);
     if (c->world == 1) return SPMV_OK;
     if (D->n_send) dist_pack<<<sm_count * 2, 256, 0, st>>>(D->d_G, D->d_sidx, D->d_S, D->n_send, ctrl);
+    if (c->lb) {
+        // rank q's segment for us sits at q's soff[rank]; it lands at our roff[q]
+        const int me = D->rank;
+        return loopback_pull(c, D->d_S, D->soff.data(), [&](int, const int64_t* offs) { return offs[me]; },
+                             [&](int q) { return D->roff[q]; }, [&](int q) { return D->rcnt[q]; }, D->d_G, st);
+    }
     spmv_status s = nccl_status(g_nccl.GroupStart(), "ncclGroupStart");
     for (int q = 0; q < D->P && !s; ++q) {
         if (q == D->rank) continue;
@@ -370,6 +464,14 @@ spmv_status exchange(spmv_comm c, Dist* D, const tc::Ctrl* ctrl, int sm_count, c
 // metadata allgather of the local-input variant (host vectors through device buffers, NCCL)
 static spmv_status allgather_host(spmv_comm c, const void* mine, void* all, size_t count, int dtype, size_t esize) {
     if (c->world == 1) { std::memcpy(all, mine, count * esize); return SPMV_OK; }
+    if (c->lb) {
+        Loopback& L = *c->lb;
+        L.host[c->rank].assign((const char*)mine, (const char*)mine + count * esize);
+        L.barrier();
+        for (int q = 0; q < c->world; ++q) std::memcpy((char*)all + (size_t)q * count * esize, L.host[q].data(), count * esize);
+        L.barrier();
+        return SPMV_OK;
+    }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, count * esize * c->world);
     if (e) return cuda_status(e, "metadata buffer");
@@ -658,7 +760,17 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     Ctrl* hc = nullptr;
     cudaMallocHost(&hc, sizeof(Ctrl));
     const int batch = 8;
+    const int cap = std::max(s->it.max_iter, s->it.fixed_iters) + batch;
     int launched = 0;
+    // an event after every enqueued iteration: the reported time ends at the iteration that
+    // converged, not at the batch's trailing (no-op kernels, but real exchanges) iterations
+    std::vector<cudaEvent_t> ev_it;
+    auto mark_iter = [&]() {
+        cudaEvent_t v;
+        cudaEventCreate(&v);
+        cudaEventRecord(v, st);
+        ev_it.push_back(v);
+    };
     while (true) {
         for (int b = 0; b < batch; ++b) {
             const size_t nu = s->tiles_used.size();
@@ -678,6 +790,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                 hits_dist_post<<<g, 512, 0, st>>>(zslot, s->d_p, D->d_half_local, D->n_local, s->d_ctrl, s->d_slots,
                                                   reinterpret_cast<double*>(zslot + D->S) + 2);
                 hits_dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, D->d_col_half, p->d_xp, D->nzc, s->d_ctrl);
+                mark_iter();
                 ++launched;
                 continue;
             }
@@ -696,18 +809,28 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
             if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
             dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->d_part_off, D->P, s->d_ctrl, rwr);
             dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+            mark_iter();
             ++launched;
         }
         cudaMemcpyAsync(hc, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
-        if ((e = cudaStreamSynchronize(st))) { cudaFreeHost(hc); return cuda_status(e, "iteration loop"); }
-        if (hc->done || launched > s->it.max_iter + batch) break;
+        if ((e = cudaStreamSynchronize(st))) {
+            cudaFreeHost(hc);
+            for (auto v : ev_it) cudaEventDestroy(v);
+            return cuda_status(e, "iteration loop");
+        }
+        if (hc->done || launched > cap) break;
     }
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
     c = *hc;
+    // PageRank / RWR: iteration k ends with the k-th body; HITS decides to stop one body later
+    // (the stop check lags one SpMV), so its converged run ends with body iter + 1
+    int64_t last = hitsa ? (int64_t)c.iter : (int64_t)c.iter - 1;
+    last = std::min<int64_t>(std::max<int64_t>(last, 0), (int64_t)ev_it.size() - 1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, last >= 0 ? ev_it[last] : e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    for (auto v : ev_it) cudaEventDestroy(v);
     cudaFreeHost(hc);
     s->last = c;
     if (res) {
