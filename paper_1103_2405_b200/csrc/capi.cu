@@ -102,15 +102,6 @@ static void free_device(spmv_plan_s* p) {
     cudaSetDevice(cur);
 }
 
-// Streaming kernel buffers: the largest workload of the plan sets the per-warp buffer size.
-static cudaError_t build_stream_tables(spmv_plan_s* p) {
-    int64_t maxspan = 0;
-    for (const auto& d : p->L.desc) maxspan = std::max<int64_t>(maxspan, (int64_t)d.h * d.w);
-    p->stage_slots = (int32_t)std::max<int64_t>(64, (maxspan + 3) / 4 * 4);
-    p->stream_grid = p->sm_count;
-    return cudaSuccess;
-}
-
 // the device work queue: descriptors in queue order
 static std::vector<PbItem> pb_queue(const PbLayout& B) {
     std::vector<PbItem> q(B.items.size());
@@ -284,14 +275,6 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
             (e = upload(&p->d_sched, zs, b)) ||
             (e = upload(&p->d_xp, xpz, b))) {
             free_device(p); delete p; return cuda_status(e, "plan upload");
-        }
-        if (const char* h = std::getenv("TCSPMV_L1_HOT")) p->l1_hot_cols = std::atoi(h);
-        if (const char* h = std::getenv("TCSPMV_PREFIX")) p->x_prefix = std::atoi(h) / 4 * 4;
-        if (const char* h = std::getenv("TCSPMV_CARVEOUT")) p->l1_carveout = std::atoi(h);
-        const char* kenv = std::getenv("TCSPMV_KERNEL");
-        p->stream = kenv && std::string(kenv) == "stream";
-        if (p->stream && (e = build_stream_tables(p))) {
-            free_device(p); delete p; return cuda_status(e, "stage tables");
         }
         if ((e = setup_grids<EpiStore>(*p, p->grid_tile))) {
             free_device(p); delete p; return cuda_status(e, "occupancy");
@@ -542,8 +525,7 @@ spmv_status spmv_execute_host_batch(spmv_plan p, const float* xh, float* yh, int
             if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_status(e, "event");
     }
     cudaEvent_t* h2d_done = p->ev_pipe;       // x buffer k filled
-    int NP = spmv_plan_s::kPipe;                   // buffer pairs in use (TCSPMV_PIPE = 2 or 3)
-    if (const char* v = std::getenv("TCSPMV_PIPE")) NP = std::max(2, std::min(spmv_plan_s::kPipe, std::atoi(v)));
+    const int NP = spmv_plan_s::kPipe;             // buffer pairs in use
     constexpr int KP = spmv_plan_s::kPipe;
     cudaEvent_t* comp_done = p->ev_pipe + KP;      // product on buffer pair k finished (x free, y ready)
     cudaEvent_t* d2h_done = p->ev_pipe + 2 * KP;   // y buffer k drained
@@ -660,7 +642,7 @@ spmv_status spmv_plan_stats(spmv_plan p, spmv_plan_stats_t* o) {
         o->tile_col_lo[t] = ti.col_lo; o->tile_col_hi[t] = ti.col_hi; o->tile_staged[t] = ti.staged;
         o->tile_predicted_us[t] = ti.pred_us; o->composite_threshold[t] = ti.threshold;
     }
-    o->resident_warps = p->grid_tile.empty() ? 0 : p->grid_tile.back() * (p->stream ? kStreamThreads / 32 : kWarps);
+    o->resident_warps = p->grid_tile.empty() ? 0 : p->grid_tile.back() * kWarps;
     o->perf_table_loaded = p->perf_table_loaded;
     o->two_phase = p->two_phase ? 1 : 0;
     o->pb_groups = p->pb_groups; o->pb_chunks = p->pb_chunks; o->pb_bins = p->pb_bins; o->pb_long_bins = p->pb_long;

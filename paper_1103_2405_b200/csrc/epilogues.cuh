@@ -13,6 +13,7 @@ template <int NP>
 __device__ __forceinline__ void block_reduce_to_slot(double (&v)[NP], double* slot) {
     __shared__ double red[kWarps][NP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncwarp();
     #pragma unroll
     for (int k = 0; k < NP; ++k)
         for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);

@@ -42,14 +42,6 @@ struct spmv_plan_s {
     uint32_t* d_sched = nullptr;    // [(kDynQ + 1) * (num_tiles + 1)] dynamic-schedule counters
     int64_t device_bytes = 0;
     int sm_count = 0;
-    // streaming kernel (per-warp bulk-copy double buffers)
-    bool stream = true;
-    int32_t stage_slots = 0;                  // slots per warp buffer (largest workload)
-    int stream_grid = 0;
-    int32_t l1_carveout = -1;              // TCSPMV_CARVEOUT: preferred shared-memory carve-out (%)
-    int32_t x_prefix = 0;                  // unstaged tiles: x columns staged in shared memory
-    int32_t l1_hot_cols = 0;               // see TileArgs::hot; 0 = plain ld.global.nc (TCSPMV_L1_HOT)
-    int max_dyn_smem = 0;
     std::vector<int> grid_tile;     // per tile persistent grid for EpiStore
     // two-phase tiles (pb.h): when set, the plan has no one-pass tiles; d_row_id holds the
     // two-phase row order (row | FLAG_FINAL, n_row_entries = n_rows) for the epilogues

@@ -60,14 +60,8 @@ namespace tc {
                            // 2 ahead keeps ~77 MB of future slots in L2 and evicts x (955 MB of
                            // DRAM reads per SpMV); at start: 635 MB (algorithmic: 610 MB), -8 % time
 #endif
-#ifndef TC_PF_POLICY
-#define TC_PF_POLICY 0     // 1: prefetched slot lines enter L2 evict-first
-#endif
 #ifndef TC_X_POLICY
 #define TC_X_POLICY 1      // 1: x gathers carry an L2 evict-last policy (x stays resident); -3 %
-#endif
-#ifndef TC_PIPE
-#define TC_PIPE 0          // 1: software-pipelined batches (next batch's slot loads overlap this batch's gathers)
 #endif
 #ifndef TC_MINB
 #define TC_MINB 2          // minimum resident CTAs per SM (__launch_bounds__)
@@ -84,10 +78,6 @@ struct TileArgs {
     const uint32_t* row_id;
     const float* x;           // x' + col_lo: tile-relative base of the relabelled x
     int32_t width;            // tile width = padding sentinel
-    int32_t hot;              // unstaged tiles: columns below are gathered with L1 evict-last,
-                              // the rest evict-first (the relabelled hub columns stay in L1)
-    int32_t prefix;           // unstaged tiles: the first `prefix` columns (the tile's densest,
-                              // Solution 2 order) are staged in shared memory, the rest gathered
     const int32_t* split;     // [n_split][3]
     float* partials;          // [n_chunks]
     int32_t* counters;        // [n_split], zero between launches
@@ -96,30 +86,13 @@ struct TileArgs {
 
 // Slot loads: SMEM = false streams from global memory with evict-first (ld.global.cs); SMEM = true
 // reads slots the bulk-copy ring already placed in shared memory.
-#ifndef TC_STREAM_NA
-#define TC_STREAM_NA 0     // 1: 128-bit slot loads bypass L1 (L1::no_allocate), leaving L1 to x
-#endif
 template <bool SMEM> __device__ __forceinline__ int4 ld_i4(const int32_t* p) {
     if (SMEM) return *reinterpret_cast<const int4*>(p);
-#if TC_STREAM_NA
-    int4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    return r;
-#else
     return __ldcs(reinterpret_cast<const int4*>(p));
-#endif
 }
 template <bool SMEM> __device__ __forceinline__ float4 ld_f4(const float* p) {
     if (SMEM) return *reinterpret_cast<const float4*>(p);
-#if TC_STREAM_NA
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-#else
     return __ldcs(reinterpret_cast<const float4*>(p));
-#endif
 }
 template <bool SMEM> __device__ __forceinline__ int2 ld_i2(const int32_t* p) {
     if (SMEM) return *reinterpret_cast<const int2*>(p);
@@ -148,33 +121,19 @@ struct XSrc {
     const float* g;     // global base (tile-relative)
     const float* s;     // shared base
     int32_t width;
-    int32_t hot;
-    int32_t prefix;
     uint64_t pol = 0;   // TC_X_POLICY: L2 evict-last policy for the gathers
     __device__ __forceinline__ float operator()(int32_t c) const {
         if (c == width) return 0.0f;                  // padding slot (sentinel, reading R16)
         if (STAGED) return s[c];
-        if (c < prefix) return s[c];
 #if TC_X_POLICY
-        {
-            float v;
-            if (hot <= 0) asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
-            else if (c < hot) asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
-            else asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
-            return v;
-        }
-#endif
-        if (hot <= 0) return __ldg(g + c);
         float v;
-        if (c < hot) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
-        else asm volatile("ld.global.nc.L1::evict_first.f32 %0, [%1];" : "=f"(v) : "l"(g + c));
+        asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(g + c), "l"(pol));
         return v;
+#else
+        return __ldg(g + c);
+#endif
     }
 };
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
 
 // one vector of KV slots: load cols (+vals), gather x, return the partial dot product
 template <int KV, bool VALUED, bool SMEM>
@@ -290,29 +249,6 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
         typename Epi::Pre pre_s[UB];
         #pragma unroll
         for (int j = 0; j < UB; ++j) pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j], eix_s[j]);
-#if TC_PIPE == 2
-        // the next batch's slot lines are pulled into L1 (no registers held) while this batch gathers
-        if (!SMEM) {
-            #pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                const int v = v0 + UB + j;
-                const int step = v / upl, q = sl + (v - step * upl) * lpr;
-                const int r = step * rps + sub;
-                if (v < V && r < d.h && q < w4) {
-                    prefetch_l1(wc + r * d.w + 4 * q);
-                    if (VALUED) prefetch_l1(wv + r * d.w + 4 * q);
-                }
-            }
-        }
-#endif
-#if TC_PIPE == 1
-        // software pipeline: the next batch's slot loads are in flight while this batch gathers
-        Unit<4, VALUED, SMEM> un[UB];
-        bool okn[UB];
-        uint32_t ent_n[UB];
-        int32_t eix_n[UB];
-        issue(v0 + UB, un, okn, ent_n, eix_n);
-#endif
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int v = v0 + j;
@@ -328,12 +264,7 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
                 acc = 0.0f;
             }
         }
-#if TC_PIPE == 1
-        #pragma unroll
-        for (int j = 0; j < UB; ++j) { u[j] = un[j]; ok[j] = okn[j]; ent_s[j] = ent_n[j]; eix_s[j] = eix_n[j]; }
-#else
         issue(v0 + UB, u, ok, ent_s, eix_s);
-#endif
     }
 }
 
@@ -370,23 +301,6 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
         typename Epi::Pre pre[UB];
         #pragma unroll
         for (int j = 0; j < UB; ++j) pre[j] = epi.prefetch(ent[j], d.row_base + lane + 32 * ((u0 + j) / nk));
-#if TC_PIPE == 2
-        if (!SMEM) {
-            #pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                const int q = u0 + UB + j;
-                if (q < total) {
-                    prefetch_l1(cb + q * (32 * KV));
-                    if (VALUED) prefetch_l1(vb + q * (32 * KV));
-                }
-            }
-        }
-#endif
-#if TC_PIPE == 1
-        Unit<KV, VALUED, SMEM> un[UB];
-        uint32_t entn[UB];
-        issue(u0 + UB, un, entn);
-#endif
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int uu = u0 + j;
@@ -397,12 +311,7 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
                 acc = 0.0f;
             }
         }
-#if TC_PIPE == 1
-        #pragma unroll
-        for (int j = 0; j < UB; ++j) { u[j] = un[j]; ent[j] = entn[j]; }
-#else
         issue(u0 + UB, u, ent);
-#endif
     }
 }
 
@@ -456,14 +365,8 @@ __device__ __forceinline__ void prefetch_workload(const TileArgs& a, int64_t j) 
     const WlDesc d = load_desc(a.desc + j);
     const uint32_t bytes = (uint32_t)((int64_t)d.h * d.w * 4 + 15) & ~15u;
     if (bytes == 0) return;
-#if TC_PF_POLICY
-    const uint64_t pol = policy_evict_first();
-    bulk_prefetch_l2_hint(a.col + d.off, bytes, pol);
-    if (VALUED) bulk_prefetch_l2_hint(a.val + d.off, bytes, pol);
-#else
     bulk_prefetch_l2(a.col + d.off, bytes);
     if (VALUED) bulk_prefetch_l2(a.val + d.off, bytes);
-#endif
 }
 
 template <bool STAGED, bool VALUED, class Epi>
@@ -471,10 +374,10 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
     extern __shared__ float xs[];
     Epi epi = epi_in;
     if (!epi.begin()) return;                         // iteration loop already converged
-    if (STAGED || a.prefix > 0) {
-        // stage the tile's x segment (or its dense prefix) once per CTA (float4 where aligned)
+    if (STAGED) {
+        // stage the tile's x segment once per CTA (float4 where aligned)
         const float* src = a.x;
-        const int n = STAGED ? a.width : a.prefix;
+        const int n = a.width;
         const int head = (int)((4 - ((reinterpret_cast<uintptr_t>(src) >> 2) & 3)) & 3);
         const int h = head < n ? head : n;
         for (int i = threadIdx.x; i < h; i += kThreads) xs[i] = __ldg(src + i);
@@ -487,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         for (int i = h + 4 * n4 + threadIdx.x; i < n; i += kThreads) xs[i] = __ldg(src + i);
         __syncthreads();
     }
-    XSrc<STAGED> x{a.x, xs, a.width, a.hot, STAGED ? 0 : a.prefix};
+    XSrc<STAGED> x{a.x, xs, a.width};
 #if TC_X_POLICY
     x.pol = policy_evict_last();
 #endif
@@ -535,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         if (kPrefetchAhead > 0 && lane == 0 && jf < n_wl) prefetch_workload<VALUED>(a, a.wl_begin + jf);
         jc = __shfl_sync(0xffffffffu, jf, 0);
     }
+    __syncwarp();                                         // converged warps at the block barrier
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -560,76 +464,6 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
 #endif
     epi.end();
 }
-
-constexpr int kStreamThreads = 512;                 // up to 16 warps per CTA
-
-// ---------------------------------------------------------------------------------------------
-// Streaming kernel (default): every warp runs its workloads (round-robin over a persistent grid)
-// out of a private double buffer in shared memory.  While the warp computes workload j from one
-// buffer, its lane 0 has already issued the 1-D bulk copies (cp.async.bulk: the TMA engine,
-// SASS UBLKCP) of the slots of its next workload into the other buffer, completion tracked by an
-// mbarrier.  The slot stream therefore never sits on the warp's dependency chain: HBM latency is
-// hidden by the copy engine, not by registers, and the warp only waits on x gathers (shared
-// memory for dense tiles, L1/L2 for the remainder).  Dense tiles also bulk-copy their x segment.
-struct WsArgs {
-    int32_t buf_slots;          // slots per buffer (>= every workload of the tile, multiple of 4)
-    int32_t x_floats;           // staged x floats (multiple of 4), 0 when not staged
-};
-
-template <bool VALUED>
-__device__ __forceinline__ void ws_issue(const TileArgs& a, const WlDesc& d, int32_t* cbuf,
-                                         float* vbuf, uint64_t* bar, uint64_t pol) {
-    const uint32_t bytes = (uint32_t)((int64_t)d.h * d.w) * 4u;
-    if (bytes == 0) { mbar_arrive(bar); return; }
-    mbar_arrive_expect_tx(bar, VALUED ? 2u * bytes : bytes);
-    bulk_g2s(cbuf, a.col + d.off, bytes, bar, pol);
-    if (VALUED) bulk_g2s(vbuf, a.val + d.off, bytes, bar, pol);
-}
-
-template <bool STAGED, bool VALUED, class Epi>
-__global__ void __launch_bounds__(kStreamThreads, 1) tc_spmv_wstream(TileArgs a, WsArgs s, Epi epi_in) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int nwarps = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                 // [nwarps][2] + x
-    uint64_t* xbar = bars + 2 * nwarps;
-    float* xs = reinterpret_cast<float*>(smem + ((2 * nwarps + 1) * 8 + 127) / 128 * 128);
-    const size_t per_buf = (size_t)s.buf_slots * (VALUED ? 2 : 1);
-    int32_t* wb = reinterpret_cast<int32_t*>(xs + s.x_floats) + (size_t)warp * 2 * per_buf;
-    Epi epi = epi_in;
-    if (!epi.begin()) return;                            // iteration loop already converged
-    if (lane == 0) { mbar_init(bars + 2 * warp, 1); mbar_init(bars + 2 * warp + 1, 1); }
-    if (threadIdx.x == 0) mbar_init(xbar, 1);
-    fence_barrier_init();
-    __syncthreads();
-    if (STAGED && threadIdx.x == 0) {
-        mbar_arrive_expect_tx(xbar, (uint32_t)s.x_floats * 4u);
-        bulk_g2s(xs, a.x, (uint32_t)s.x_floats * 4u, xbar, policy_evict_last());
-    }
-    const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
-    const int64_t G = (int64_t)gridDim.x * nwarps;
-    const uint64_t pol = policy_evict_first();
-    int32_t* cbuf[2] = {wb, wb + per_buf};
-    float* vbuf[2] = {reinterpret_cast<float*>(wb + s.buf_slots), reinterpret_cast<float*>(wb + per_buf + s.buf_slots)};
-    int64_t j = a.wl_begin + gw;
-    WlDesc d = j < a.wl_end ? load_desc(a.desc + j) : WlDesc{};
-    if (lane == 0 && j < a.wl_end) ws_issue<VALUED>(a, d, cbuf[0], vbuf[0], bars + 2 * warp, pol);
-    if (STAGED) mbar_wait(xbar, 0);
-    XSrc<STAGED> x{a.x, xs, a.width, a.hot, 0};
-    for (int k = 0; j < a.wl_end; j += G, ++k) {
-        const int cur = k & 1;
-        const int64_t jn = j + G;
-        WlDesc dn = jn < a.wl_end ? load_desc(a.desc + jn) : WlDesc{};
-        if (lane == 0 && jn < a.wl_end) ws_issue<VALUED>(a, dn, cbuf[cur ^ 1], vbuf[cur ^ 1], bars + 2 * warp + (cur ^ 1), pol);
-        mbar_wait(bars + 2 * warp + cur, (uint32_t)(k >> 1) & 1u);
-        run_workload<VALUED, true>(a, d, cbuf[cur], VALUED ? vbuf[cur] : nullptr, x, epi, lane);
-        __syncwarp();                                    // buffer `cur` is refilled two workloads on
-        d = dn;
-    }
-    epi.end();
-}
-
-__host__ __device__ constexpr int ws_bar_bytes(int nwarps) { return ((2 * nwarps + 1) * 8 + 127) / 128 * 128; }
 
 // Epilogue interface: prefetch(ent, e) loads what the row's write needs (the partial sum of
 // earlier tiles when FLAG_ACC, epilogue operands) early; commit(ent, e, v, pre) stores the row's
