@@ -202,6 +202,10 @@ typedef struct {
     int32_t exchange;      /* multi-GPU only: 0 = one allgather of every non-empty column (default);
                             * 1 = needed columns: each rank receives only the values its rows read,
                             *     by grouped NCCL send/recv (spmv_needed_lists) */
+    int32_t host_loop;     /* single GPU: 0 = the iterations run as a CUDA graph with a device-side
+                            * WHILE loop (default); 1 = the host enqueues them in batches of 8 and
+                            * reads the device's stop flag (same kernels and results; for profilers
+                            * and sanitizers, which do not see inside conditional graph nodes) */
 } spmv_iter_opts;
 void spmv_iter_opts_default(spmv_iter_opts* o, int algo);
 

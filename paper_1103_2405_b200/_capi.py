@@ -54,7 +54,7 @@ class LayoutView(ctypes.Structure):
 
 class IterOpts(ctypes.Structure):
     _fields_ = [("c", c_f64), ("tol", c_f64), ("max_iter", c_i32), ("hits_norm", c_i32),
-                ("fixed_iters", c_i32), ("exchange", c_i32)]
+                ("fixed_iters", c_i32), ("exchange", c_i32), ("host_loop", c_i32)]
 
 
 class IterResult(ctypes.Structure):

@@ -1,10 +1,12 @@
 // batch.cu -- batched Random Walk with Restart (the
 // paper averages 25 random query nodes).  The Q <= 32 queries iterate together as one SpMM
-// Y = W R over the same tiled-composite layout: lanes are queries, so every stored entry costs one
-// coalesced 128-byte read of an x row (all queries' values of that column) instead of a random
-// 4-byte gather per query.  Rows are written as 128-byte rows too.  Everything else (tiles in
-// fixed order, first-touch/accumulate flags, split chunks combined in chunk order, fp64 per-query
-// partial sums reduced in a fixed order, device-side WHILE loop) follows the single-query path.
+// Y = W R over a row-major-only (CSR-vector, f2) tiled-composite layout of the same matrix: lanes
+// are queries, so every stored entry costs one coalesced 128-byte read of an x row (all queries'
+// values of that column) instead of a random 4-byte gather per query.  A warp walks a workload's
+// slots as one flat stream with 16 x-row loads in flight whatever the row lengths, and writes
+// each finished row of Y (stores only); Eq. 9 runs as a separate streaming pass over the N x 32
+// rows (spmm_rwr_epilogue: r' = c y + (1-c) e_q, z' = r' / deg, per-query fp64 L1 change reduced
+// in a fixed order), then the device-side WHILE loop decides.  Split rows combine in chunk order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +23,7 @@
 namespace tc {
 
 constexpr int kQP = 32;                 // padded queries per row (one per lane)
+constexpr int kBatchCtasPerSm = 2;      // spmm_rwr_tile: 2 x 512 threads per SM (<= 64 registers)
 
 struct BatchArgs {
     const WlDesc* desc;
@@ -46,21 +49,17 @@ struct BatchArgs {
     cudaGraphConditionalHandle cond;
 };
 
+// The SpMM writes the product Y = W_pattern Z only (first touch stores, later tiles add): its
+// stores need no response, so a warp's gathers never wait on epilogue traffic.  Eq. 9 is applied
+// by spmm_rwr_epilogue, a streaming pass over the N x 32 rows.
 struct BatchEpi {
     const BatchArgs& a;
     int lane;
-    double& res;
     __device__ __forceinline__ void write(uint32_t ent, float v) {
         if (ent == PAD_ROW) return;
-        const uint32_t r = ent & ROW_MASK;
-        const int64_t o = (int64_t)r * kQP + lane;
+        const int64_t o = (int64_t)(ent & ROW_MASK) * kQP + lane;
         if (ent & FLAG_ACC) v += a.Y[o];
-        if (!(ent & FLAG_FINAL)) { a.Y[o] = v; return; }
-        float rn = a.c * v;
-        if ((int32_t)r == a.q[lane]) rn += 1.0f - a.c;       // Eq. 9: + (1-c) e_q
-        res += fabs((double)rn - (double)a.R[o]);
-        a.R[o] = rn;
-        a.Znext[o] = rn * __ldg(a.inv + r);
+        a.Y[o] = v;
     }
 };
 
@@ -69,108 +68,192 @@ __device__ __forceinline__ float xrow(const BatchArgs& a, int32_t c, int lane) {
     return __ldg(a.Z + (a.col_lo + c) * kQP + lane);
 }
 
-// one row of `len` slots starting at cb (row major / split chunk); all lanes see every slot
-__device__ __forceinline__ float row_dot(const BatchArgs& a, const int32_t* cb, int len, int lane) {
+#ifndef TC_BATCH_U
+#define TC_BATCH_U 16
+#endif
+constexpr int kRowU = TC_BATCH_U;       // x-row loads in flight per warp step
+
+// row rr of a column-major 32-row slab (k-interleaved by kvec): its w slots sit at
+// sb + (k / kvec) * 32 kvec + rr kvec + k % kvec; 32 ids per warp load, then as row_dot
+__device__ __forceinline__ float slab_row_dot(const BatchArgs& a, const int32_t* sb, int rr, int w, int kvec,
+                                              int lane) {
     float acc = 0.0f;
-    for (int k0 = 0; k0 < len; k0 += 32) {
-        const int32_t cl = (k0 + lane < len) ? __ldcs(cb + k0 + lane) : a.width;
-        // all 32 x rows of the chunk in flight before the sum (padding -> sentinel -> 0)
-        float xv[32];
-        #pragma unroll
-        for (int j = 0; j < 32; ++j) xv[j] = xrow(a, __shfl_sync(0xffffffffu, cl, j), lane);
-        #pragma unroll
-        for (int j = 0; j < 32; ++j) acc += xv[j];
+    for (int k0 = 0; k0 < w; k0 += 32) {
+        const int k = k0 + lane;
+        const int32_t cl = k < w ? __ldg(sb + (k / kvec) * 32 * kvec + rr * kvec + k % kvec) : a.width;
+        const int n = min(32, w - k0);
+        for (int j0 = 0; j0 < n; j0 += kRowU) {
+            float xv[kRowU];
+            #pragma unroll
+            for (int t = 0; t < kRowU; ++t) xv[t] = xrow(a, __shfl_sync(0xffffffffu, cl, j0 + t), lane);
+            #pragma unroll
+            for (int t = 0; t < kRowU; ++t) acc += xv[t];
+        }
     }
     return acc;
 }
 
-template <int KV>
-__device__ __forceinline__ void slab_round(const BatchArgs& a, const int32_t* sb, int p0, float (&acc)[32], int lane) {
-    // positions p0 .. p0+31 of a k-interleaved slab: row rr = (p % (32 KV)) / KV
-    const int32_t cl = __ldcs(sb + p0 + lane);
-    const int base = (p0 % (32 * KV)) / KV;
-    float xv[32];
-    #pragma unroll
-    for (int j = 0; j < 32; ++j) xv[j] = xrow(a, __shfl_sync(0xffffffffu, cl, j), lane);
-    // rr = base + j / KV, with base in {0, 32/KV, ...}: dispatch on base keeps acc indices static
-    #pragma unroll
-    for (int b = 0; b < KV; ++b) {
-        if (base != b * (32 / KV)) continue;
-        #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[b * (32 / KV) + j / KV] += xv[j];
+// a split chunk's partial; the last chunk to arrive sums the row's chunks in chunk order
+__device__ __forceinline__ void split_write(const BatchArgs& a, const WlDesc& d, uint32_t ent, float v,
+                                            BatchEpi& epi, int lane) {
+    const int32_t* sp = a.split + 3 * d.split_id;
+    const int32_t nch = __ldg(sp + 1), pbase = __ldg(sp + 2);
+    a.partials[(int64_t)(pbase + d.chunk) * kQP + lane] = v;
+    __threadfence();
+    __syncwarp();
+    int32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.counters + d.split_id, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t == nch - 1) {
+        __threadfence();
+        float s = 0.0f;
+        for (int32_t c = 0; c < nch; ++c) s += __ldcg(a.partials + (int64_t)(pbase + c) * kQP + lane);
+        __syncwarp();
+        if (lane == 0) a.counters[d.split_id] = 0;
+        epi.write(ent, s);
     }
 }
 
-__global__ void __launch_bounds__(512, 1) spmm_rwr_tile(BatchArgs a) {
+__global__ void __launch_bounds__(512, 2) spmm_rwr_tile(BatchArgs a) {
     if (*(volatile int32_t*)&a.ctrl->done) return;
     const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * warps;
-    double res = 0.0;
-    BatchEpi epi{a, lane, res};
+    BatchEpi epi{a, lane};
+    // this lane's query column of the tile's x rows (plain L2 caching: evict-last / evict-first
+    // hints on the hub / tail rows measured slower on c2, 5.5-6.6 vs 4.3 ms per iteration)
+    const float* zl = a.Z + a.col_lo * kQP + lane;
     for (int64_t j = a.wl_begin + gw; j < a.wl_end; j += G) {
         const WlDesc d = load_desc(a.desc + j);
         const int32_t* wc = a.col + d.off;
         if (d.kind != KIND_CM) {
-            for (int r = 0; r < d.h; ++r) {
-                const float v = row_dot(a, wc + (int64_t)r * d.w, d.w, lane);
-                const uint32_t ent = __ldg(a.row_id + d.row_base + r);
-                if (d.kind == KIND_SPLIT) {
-                    const int32_t* sp = a.split + 3 * d.split_id;
-                    const int32_t nch = __ldg(sp + 1), pbase = __ldg(sp + 2);
-                    a.partials[(int64_t)(pbase + d.chunk) * kQP + lane] = v;
-                    __threadfence();
-                    __syncwarp();
-                    int32_t t = 0;
-                    if (lane == 0) t = atomicAdd(a.counters + d.split_id, 1);
-                    t = __shfl_sync(0xffffffffu, t, 0);
-                    if (t == nch - 1) {
-                        __threadfence();
-                        float s = 0.0f;
-                        for (int32_t c = 0; c < nch; ++c) s += __ldcg(a.partials + (int64_t)(pbase + c) * kQP + lane);
-                        __syncwarp();
-                        if (lane == 0) a.counters[d.split_id] = 0;
-                        epi.write(ent, s);
-                    }
-                } else {
-                    epi.write(ent, v);
+            // the workload's h rows of w slots as one flat stream: kRowU x-row loads in flight per
+            // step whatever the row lengths; a row ends every w slots (warp-uniform)
+            const int total = d.h * d.w;
+            float acc = 0.0f;
+            int32_t cl = (lane < total) ? __ldcs(wc + lane) : a.width;   // ids of slots [s0, s0 + 32)
+            int32_t cn = a.width;
+            int row = 0, next_end = d.w;                  // slot after the current row
+            for (int s0 = 0; s0 < total; s0 += kRowU) {
+                const int base = s0 & 31;
+                // the next 32 ids are requested a step ahead of their use
+                if (base == 0) cn = (s0 + 32 + lane < total) ? __ldcs(wc + s0 + 32 + lane) : a.width;
+                float xv[kRowU];
+                #pragma unroll
+                for (int t = 0; t < kRowU; ++t) {
+                    const int32_t c = __shfl_sync(0xffffffffu, cl, base + t);
+                    xv[t] = c != a.width ? __ldg(zl + (int64_t)c * kQP) : 0.0f;
                 }
+                if (next_end - s0 > kRowU) {              // no row ends in this step (warp-uniform)
+                    #pragma unroll
+                    for (int t = 0; t < kRowU; ++t) acc += xv[t];
+                } else {
+                    #pragma unroll
+                    for (int t = 0; t < kRowU; ++t) {
+                        if (s0 + t >= total) break;
+                        acc += xv[t];
+                        if (s0 + t + 1 == next_end) {
+                            const uint32_t ent = __ldg(a.row_id + d.row_base + row);
+                            if (d.kind == KIND_SPLIT) split_write(a, d, ent, acc, epi, lane);
+                            else epi.write(ent, acc);
+                            acc = 0.0f;
+                            ++row;
+                            next_end += d.w;
+                        }
+                    }
+                }
+                if (base + kRowU == 32) cl = cn;
             }
         } else {
+            // column major (zero-length rows of the remainder; the batch plan is row major only)
             const int slabs = d.h >> 5;
-            for (int s = 0; s < slabs; ++s) {
-                float acc[32];
-                #pragma unroll
-                for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
-                const int32_t* sb = wc + (int64_t)s * 32 * d.w;
-                const int npos = 32 * d.w;
-                for (int p0 = 0; p0 < npos; p0 += 32) {
-                    if (d.kvec == 4) slab_round<4>(a, sb, p0, acc, lane);
-                    else if (d.kvec == 2) slab_round<2>(a, sb, p0, acc, lane);
-                    else slab_round<1>(a, sb, p0, acc, lane);
+            for (int sl = 0; sl < slabs; ++sl) {
+                const int32_t* sb = wc + (int64_t)sl * 32 * d.w;
+                const uint32_t myent = __ldg(a.row_id + d.row_base + sl * 32 + lane);
+                for (int rr = 0; rr < 32; ++rr) {
+                    const float v = slab_row_dot(a, sb, rr, d.w, d.kvec, lane);
+                    epi.write(__shfl_sync(0xffffffffu, myent, rr), v);
                 }
-                const uint32_t myent = __ldg(a.row_id + d.row_base + s * 32 + lane);
-                #pragma unroll
-                for (int rr = 0; rr < 32; ++rr) epi.write(__shfl_sync(0xffffffffu, myent, rr), acc[rr]);
             }
         }
     }
-    // per-query residual: fixed-order block reduction over warps, then over blocks
+}
+
+// Eq. 9 over every (row, query): r' = c y + (1 - c) e_q, z' = r' / deg; per-query L1 change in
+// fp64, reduced in a fixed order (per block over warps, then the last block over blocks).
+__global__ void __launch_bounds__(512) spmm_rwr_epilogue(BatchArgs a, int64_t N) {
+    if (*(volatile int32_t*)&a.ctrl->done) return;
+    const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    // thread = 4 queries (one float4) of a row; a warp covers 4 rows per step, 4 steps in flight
+    const int g = lane & 7, sub = lane >> 3;
+    int32_t q[4];
+    #pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = a.q[4 * g + k];
+    double rk[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t wid = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5), W = (int64_t)gridDim.x * warps;
+    constexpr int kU = 4;
+    for (int64_t r0 = 4 * wid * kU; r0 < N; r0 += 4 * W * kU) {
+        float4 y[kU], rold[kU];
+        float iv[kU];
+        #pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t r = r0 + 4 * u + sub;
+            if (r < N) {
+                y[u] = __ldcs(reinterpret_cast<const float4*>(a.Y + r * kQP) + g);
+                rold[u] = *(reinterpret_cast<const float4*>(a.R + r * kQP) + g);
+                iv[u] = __ldg(a.inv + r);
+            }
+        }
+        #pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t r = r0 + 4 * u + sub;
+            if (r >= N) continue;
+            float rn[4] = {a.c * y[u].x, a.c * y[u].y, a.c * y[u].z, a.c * y[u].w};
+            const float ro[4] = {rold[u].x, rold[u].y, rold[u].z, rold[u].w};
+            #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if ((int32_t)r == q[k]) rn[k] += 1.0f - a.c;     // Eq. 9: + (1 - c) e_q
+                rk[k] += fabs((double)rn[k] - (double)ro[k]);
+            }
+            *(reinterpret_cast<float4*>(a.R + r * kQP) + g) = make_float4(rn[0], rn[1], rn[2], rn[3]);
+            *(reinterpret_cast<float4*>(a.Znext + r * kQP) + g) =
+                make_float4(rn[0] * iv[u], rn[1] * iv[u], rn[2] * iv[u], rn[3] * iv[u]);
+        }
+    }
+    // per query 4g + k: sum the four row lanes (sub) of the warp in a fixed order
+    double res = 0.0;
+    #pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double v = rk[k];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        rk[k] = v;
+    }
+    // lane l now reports query l = 4 g + k with g = l >> 2, k = l & 3 (held by lanes g, g + 8, ...)
+    {
+        const int gq = lane >> 2, kq = lane & 3;
+        double mine = 0.0;
+        #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double v = __shfl_sync(0xffffffffu, rk[k], gq);
+            if (k == kq) mine = v;
+        }
+        res = mine;
+    }
     __shared__ double red[16][32];
     const int w = threadIdx.x >> 5;
     red[w][lane] = res;
     __syncthreads();
     if (threadIdx.x < 32) {
-        double s = 0.0;
-        for (int k = 0; k < warps; ++k) s += red[k][threadIdx.x];
-        a.slots[(int64_t)(a.slot_base + blockIdx.x) * 32 + threadIdx.x] = s;
+        double t = 0.0;
+        for (int k = 0; k < warps; ++k) t += red[k][threadIdx.x];
+        a.slots[(int64_t)blockIdx.x * 32 + threadIdx.x] = t;
     }
-    if (!a.is_last) return;
     if (!last_block(&a.ctrl->ticket)) return;
     if (threadIdx.x < 32) {
-        double s = 0.0;
-        for (int b = 0; b < a.total_slots; ++b) s += __ldcg(a.slots + (int64_t)b * 32 + threadIdx.x);
-        a.res_out[threadIdx.x] = s;
+        double t = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(a.slots + (int64_t)b * 32 + threadIdx.x);
+        a.res_out[threadIdx.x] = t;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -232,11 +315,10 @@ static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int pari
     return a;
 }
 
-// Tiling for the batch (Solution 1, where it pays on B200): a gathered x row is 128
-// bytes here, so the hub columns' rows are worth keeping in L2 -- one dense tile whose Z segment
-// takes about 40 % of L2, then the remainder.  The single-query plan stays untiled (4-byte gathers
-// are request-bound).  Built from the solver plan's layout (identical matrix; the
-// column order is the same length order, so the plan permutation stays the identity).
+// The batch's plan: one tile (x rows are 128 bytes here; a dense tile would make every row it
+// shares with the remainder a 128-byte read-modify-write, measured slower on c2), row major only.
+// Built from the solver plan's layout (identical matrix; the column order is the same length
+// order, so the plan permutation stays the identity).
 static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
     spmv_plan_s* p = s->plan;
     int64_t tw = 0;
@@ -246,7 +328,8 @@ static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s->device);
         tw = std::max<int64_t>(4096, (int64_t)(0.4 * l2) / (kQP * 4)) / 4096 * 4096;
         if (const char* e = std::getenv("TCSPMV_BATCH_TW")) tw = std::atoll(e);
-        T = p->n_cols > tw ? 1 : 0;
+        T = 0;   // one tile: a dense tile's partial rows cost a 128-byte read-modify-write each
+                 // (measured on c2: 1 tile 4.26 ms, 2 tiles 5.19 ms, 3 tiles 6.06 ms per iteration)
         if (const char* e = std::getenv("TCSPMV_BATCH_TILES")) T = std::atoi(e);
         T = (int32_t)std::min<int64_t>(T, (p->n_cols + tw - 1) / std::max<int64_t>(tw, 1));
     }
@@ -288,6 +371,10 @@ static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
     opt.num_tiles = T;
     opt.stage_x = 0;
     opt.two_phase = 0;         // the SpMM kernel runs on the one-pass tile layout
+    // row major workloads only (the CSR-vector case of the format, f2): a warp walks whole rows,
+    // each slot one 128-byte x row for all queries; rows padded to 4 slots
+    opt.orient = 1;
+    opt.align_rm = 4;
     if (opt.workload_size <= 0) opt.workload_size = p->opt.workload_size > 0 ? p->opt.workload_size : 1024;
     st = create_plan(p->n_rows, p->n_cols, p->nnz, rp.data(), col.data(), nullptr, &opt, s->device, &B->plan);
     if (st) return st;
@@ -295,6 +382,7 @@ static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
         if (B->plan->perm[k] != (int32_t)k) { set_error("internal: batch plan permutation"); return SPMV_EINVAL; }
     for (int32_t t = 0; t <= B->plan->num_tiles; ++t)
         if (B->plan->tiles[t].wl_end > B->plan->tiles[t].wl_begin) B->tiles.push_back(t);
+
     // the solver plan's host layout copy was only needed for the decode
     p->L.desc = {}; p->L.row_id = {}; p->L.slot_col = {}; p->L.slot_val = {}; p->L.split = {};
     p->host_valid = false;
@@ -304,7 +392,7 @@ static spmv_status build_batch_plan(spmv_solver_s* s, BatchState* B) {
 static cudaError_t enqueue_batch_iteration(spmv_solver_s* s, BatchState* B, int parity, cudaStream_t st,
                                            cudaGraphConditionalHandle cond) {
     const size_t nu = B->tiles.size();
-    const int sms = B->plan->sm_count;
+    const int sms = B->plan->sm_count * kBatchCtasPerSm;
     int32_t total = 0;
     for (size_t i = 0; i < nu; ++i) total += sms;
     int32_t base = 0;
@@ -315,7 +403,9 @@ static cudaError_t enqueue_batch_iteration(spmv_solver_s* s, BatchState* B, int 
         cudaError_t e = cudaGetLastError();
         if (e) return e;
     }
-    return cudaSuccess;
+    BatchArgs a = batch_args(s, B, B->tiles.empty() ? 0 : B->tiles.back(), parity, 0, 0, true, cond);
+    spmm_rwr_epilogue<<<B->plan->sm_count * 4, 512, 0, st>>>(a, B->N);
+    return cudaGetLastError();
 }
 
 extern "C" {
@@ -346,7 +436,7 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         if (bs) { batch_destroy(s); return bs; }
     }
     spmv_plan_s* p = B->plan;
-    if (!B->exec) {
+    if (!B->R) {
         const size_t vec = (size_t)(s->N + 4) * kQP * sizeof(float);
         // any failure below releases the whole batch state (buffers, graph, plan)
 #define CKB(x) do { if ((e = (x)) != cudaSuccess) { spmv_status r_ = cuda_status(e, #x); batch_destroy(s); return r_; } } while (0)
@@ -355,12 +445,14 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         CKB(cudaMalloc(&B->Z[1], vec));
         CKB(cudaMemset(B->Z[0], 0, vec));
         CKB(cudaMemset(B->Z[1], 0, vec));
-        if (p->num_tiles > 0) CKB(cudaMalloc(&B->Y, vec));
+        CKB(cudaMalloc(&B->Y, vec));
         CKB(cudaMalloc(&B->partials, (size_t)std::max<int64_t>(p->n_chunks, 1) * kQP * sizeof(float)));
         CKB(cudaMalloc(&B->q, kQP * sizeof(int32_t)));
-        const size_t nslots = (size_t)std::max<size_t>(B->tiles.size(), 1) * p->sm_count;
+        const size_t nslots = (size_t)p->sm_count * 4;
         CKB(cudaMalloc(&B->slots, nslots * kQP * sizeof(double)));
         CKB(cudaMalloc(&B->res, kQP * sizeof(double)));
+    }
+    if (!B->exec && !s->it.host_loop) {
         // device-side loop: WHILE node around two iterations (double-buffered input)
         cudaGraph_t g;
         CKB(cudaGraphCreate(&g, 0));
@@ -398,15 +490,43 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
-    e = cudaGraphLaunch(B->exec, st);
+    cudaEvent_t e_stop = nullptr;
+    if (s->it.host_loop) {
+        // host-enqueued iterations (profilers, sanitizers): batches of 8, then the stop flag
+        const int cap = std::max(s->it.max_iter, s->it.fixed_iters) + 8;
+        std::vector<cudaEvent_t> ev;
+        int launched = 0;
+        e = cudaSuccess;
+        while (!e) {
+            for (int b = 0; b < 8 && !e; ++b, ++launched) {
+                e = enqueue_batch_iteration(s, B, launched & 1, st, 0);
+                cudaEvent_t v;
+                cudaEventCreate(&v);
+                cudaEventRecord(v, st);
+                ev.push_back(v);
+            }
+            if (!e) e = cudaMemcpyAsync(&c, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+            if (!e) e = cudaStreamSynchronize(st);
+            if (e || c.done || launched > cap) break;
+        }
+        if (!e && !ev.empty()) {
+            const int64_t last = std::min<int64_t>(std::max<int64_t>(c.iter - 1, 0), (int64_t)ev.size() - 1);
+            e_stop = ev[last];
+            ev[last] = nullptr;
+        }
+        for (auto v : ev) if (v) cudaEventDestroy(v);
+    } else {
+        e = cudaGraphLaunch(B->exec, st);
+    }
     cudaEventRecord(e1, st);
     B->residual.assign(kQP, 0.0);
     if (!e) e = cudaMemcpyAsync(&c, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaMemcpyAsync(B->residual.data(), B->res, kQP * sizeof(double), cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaStreamSynchronize(st);
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventElapsedTime(&ms, e0, e_stop ? e_stop : e1);
     cudaEventDestroy(e0); cudaEventDestroy(e1);
+    if (e_stop) cudaEventDestroy(e_stop);
     if (e) return cuda_status(e, "batched loop");
     if (res) {
         res->iterations = c.iter; res->residual = c.residual;

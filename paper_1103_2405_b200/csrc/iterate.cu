@@ -183,6 +183,39 @@ static cudaError_t enqueue_iteration(spmv_solver_s* s, int parity, cudaStream_t 
     return cudaSuccess;
 }
 
+// the iteration loop without a graph: iterations (double-buffered z) enqueued in batches of 8,
+// the stop flag read after each batch; *stop = the event after the iteration that stopped
+static cudaError_t run_host_loop(spmv_solver_s* s, cudaStream_t st, cudaEvent_t* stop) {
+    const int batch = 8;
+    const int cap = std::max(s->it.max_iter, s->it.fixed_iters) + batch;
+    Ctrl* hc = nullptr;
+    cudaError_t e = cudaMallocHost(&hc, sizeof(Ctrl));
+    if (e) return e;
+    std::vector<cudaEvent_t> ev;
+    int launched = 0;
+    while (!e) {
+        for (int b = 0; b < batch && !e; ++b, ++launched) {
+            e = enqueue_iteration(s, launched & 1, st, 0);
+            cudaEvent_t v;
+            cudaEventCreate(&v);
+            cudaEventRecord(v, st);
+            ev.push_back(v);
+        }
+        if (!e) e = cudaMemcpyAsync(hc, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+        if (!e) e = cudaStreamSynchronize(st);
+        if (e || hc->done || launched > cap) break;
+    }
+    if (!e && !ev.empty()) {
+        // HITS counts an iteration per normalisation pass, one per body as well
+        const int64_t last = std::min<int64_t>(std::max<int64_t>(hc->iter - 1, 0), (int64_t)ev.size() - 1);
+        *stop = ev[last];
+        ev[last] = nullptr;
+    }
+    for (auto v : ev) if (v) cudaEventDestroy(v);
+    cudaFreeHost(hc);
+    return e;
+}
+
 static spmv_status build_graph(spmv_solver_s* s, cudaStream_t st) {
     cudaError_t e;
     cudaGraph_t g = nullptr;
@@ -218,6 +251,7 @@ __attribute__((visibility("default"))) void spmv_iter_opts_default(spmv_iter_opt
     if (!o) return;
     o->c = algo == SPMV_ALGO_RWR ? 0.9 : 0.85;
     o->tol = 1e-6; o->max_iter = 1000; o->hits_norm = 1; o->fixed_iters = 0; o->exchange = 0;
+    o->host_loop = 0;
 }
 
 __attribute__((visibility("default")))
@@ -287,7 +321,7 @@ spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_ite
             return cuda_status(e, "stream");
         st = s->own_stream;
     }
-    if (!s->exec) { spmv_status b = build_graph(s, st); if (b) return b; }
+    if (!s->exec && !s->it.host_loop) { spmv_status b = build_graph(s, st); if (b) return b; }
     Ctrl c{};
     const double n = (double)s->n;
     c.c = s->it.c; c.tol = s->it.tol; c.max_iter = s->it.max_iter; c.fixed_iters = s->it.fixed_iters;
@@ -311,16 +345,25 @@ spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_ite
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
-    e = cudaGraphLaunch(s->exec, st);
+    cudaEvent_t e_stop = nullptr;
+    if (s->it.host_loop) e = run_host_loop(s, st, &e_stop);   // the same kernels, host-enqueued
+    else e = cudaGraphLaunch(s->exec, st);
     cudaEventRecord(e1, st);
-    if (e) { cudaEventDestroy(e0); cudaEventDestroy(e1); return cuda_status(e, "cudaGraphLaunch"); }
+    if (e) {
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+        if (e_stop) cudaEventDestroy(e_stop);
+        return cuda_status(e, "iteration loop");
+    }
     if ((e = cudaMemcpyAsync(&c, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st)) ||
         (e = cudaStreamSynchronize(st))) {
-        cudaEventDestroy(e0); cudaEventDestroy(e1); return cuda_status(e, "iteration loop");
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+        if (e_stop) cudaEventDestroy(e_stop);
+        return cuda_status(e, "iteration loop");
     }
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventElapsedTime(&ms, e0, e_stop ? e_stop : e1);
     cudaEventDestroy(e0); cudaEventDestroy(e1);
+    if (e_stop) cudaEventDestroy(e_stop);
     s->last = c;
     if (res) {
         res->iterations = c.iter; res->residual = c.residual;

@@ -213,3 +213,30 @@ def test_config2_c3_skew_sweep_full_size(cfg, alpha, gpu):
     idx = np.concatenate([np.arange(G.row_ptr[r], G.row_ptr[r + 1]) for r in rows])
     yo, bo = oracle.spmv(sub_rp, G.col[idx], val[idx], x)
     assert np.all(np.abs(y[rows] - yo) <= 1e-5 * bo + 1e-30)
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "hits", "rwr"])
+def test_host_loop_matches_graph(algo, gpu):
+    """spmv_iter_opts.host_loop = 1 (host-enqueued iterations, for profilers) runs the same kernels
+    as the device-side WHILE graph: identical iterations and bitwise identical results."""
+    from paper_1103_2405_b200 import Solver
+    G = graphgen.make_graph("t_mid")
+    q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][1])
+    out = []
+    for hl in (0, 1):
+        s = Solver(algo, G.n, G.row_ptr, G.col, device=0, iter_kw=dict(host_loop=hl))
+        info = s.run(q)
+        r = s.result()
+        out.append((info["iterations"], r))
+        if algo == "rwr":
+            s.run_batch([q, q + 1, q + 2])
+            out.append(s.result_batch())
+        s.close()
+    assert out[0][0] == out[-1 if algo != "rwr" else 2][0]
+    a, b = (out[0], out[1]) if algo != "rwr" else (out[0], out[2])
+    ra = a[1] if isinstance(a[1], tuple) else (a[1],)
+    rb = b[1] if isinstance(b[1], tuple) else (b[1],)
+    for u, v in zip(ra, rb):
+        assert u.tobytes() == v.tobytes()
+    if algo == "rwr":
+        assert out[1].tobytes() == out[3].tobytes()
