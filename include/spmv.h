@@ -56,7 +56,7 @@ typedef struct spmv_solver_s* spmv_solver;
  * spmv_options_default() fills: tile_width 0 (auto), num_tiles -1 (auto), workload_size -1
  * (auto), workload_sizes NULL, align_rm 8, split_long_rows 1, camping_pad 0, pattern 0,
  * ell_h 32, stage_x 1, perf_table_path NULL, orient 0, two_phase -1, pb_region / pb_chunk /
- * pb_xcap / pb_group 0 (defaults). */
+ * pb_xcap / pb_group 0 (defaults), keep_col_order 0. */
 typedef struct {
     int32_t tile_width;      /* columns per dense tile (paper: 64K, L60); 0 = chosen by the tuner */
     int32_t num_tiles;       /* dense tiles before the remainder; -1 = auto (Alg. 1 + B200 model);
@@ -87,6 +87,11 @@ typedef struct {
     int32_t pb_xcap;         /* two-phase: columns per chunk x segment (0 = 8192; <= 65536) */
     int64_t pb_group;        /* two-phase: products per group of bins kept L2-resident between the
                                 phases (0 = chosen from the L2 size) */
+    int32_t keep_col_order;  /* 1: skip the column relabel (Solution 2) and keep the caller's
+                                column order -- for an x laid out by someone else (the row-
+                                partitioned solvers read the exchange buffer directly); no dense
+                                tiles then (Alg. 1 needs length-sorted columns), only L2-sized ones
+                                when x exceeds L2.  One-pass tiles only.  Default 0. */
 } spmv_options;
 
 void spmv_options_default(spmv_options* opt);

@@ -23,7 +23,7 @@ class Options(ctypes.Structure):
                 ("split_long_rows", c_i32), ("camping_pad", c_i32), ("pattern", c_i32),
                 ("ell_h", c_i32), ("stage_x", c_i32), ("perf_table_path", ctypes.c_char_p),
                 ("orient", c_i32), ("two_phase", c_i32), ("pb_region", c_i32), ("pb_chunk", c_i32),
-                ("pb_xcap", c_i32), ("pb_group", c_i64)]
+                ("pb_xcap", c_i32), ("pb_group", c_i64), ("keep_col_order", c_i32)]
 
 
 class PlanStats(ctypes.Structure):

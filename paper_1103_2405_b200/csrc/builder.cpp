@@ -21,7 +21,7 @@ namespace tc {
 static inline int64_t roundup(int64_t a, int64_t b) { return ((a + b - 1) / b) * b; }
 
 spmv_status prepare(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
-                    const int32_t* col, const float* val, bool pattern, Prepared& P) {
+                    const int32_t* col, const float* val, bool pattern, Prepared& P, bool keep_order) {
     if (n_rows < 0 || n_cols < 0 || nnz < 0) { set_error("negative size"); return SPMV_EINVAL; }
     if (n_rows >= (int64_t(1) << 29)) { set_error("n_rows must be < 2^29"); return SPMV_ERANGE; }
     if (n_cols > INT32_MAX - 1) { set_error("n_cols must be < 2^31-1"); return SPMV_ERANGE; }
@@ -53,7 +53,8 @@ spmv_status prepare(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* 
     P.perm.assign(n_cols, 0);
     P.inv.assign(n_cols, 0);
     for (int64_t j = 0; j < n_cols; ++j) {
-        int64_t pos = start[maxlen - len[j]]++;
+        // keep_order: the caller's column order is kept (its x is laid out by someone else)
+        int64_t pos = keep_order ? j : start[maxlen - len[j]]++;
         P.perm[pos] = (int32_t)j;
         P.inv[j] = (int32_t)pos;
     }

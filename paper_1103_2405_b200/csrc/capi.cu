@@ -203,7 +203,8 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device);
     }
     Prepared P;
-    spmv_status st = prepare(n_rows, n_cols, nnz, row_ptr, col, val, opt.pattern != 0, P);
+    if (opt.keep_col_order && opt.two_phase == 1) { set_error("keep_col_order is a one-pass option"); return SPMV_EINVAL; }
+    spmv_status st = prepare(n_rows, n_cols, nnz, row_ptr, col, val, opt.pattern != 0, P, opt.keep_col_order != 0);
     if (st) return st;
     BuildParams bp;
     std::vector<double> pred;
@@ -222,7 +223,8 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     // in auto mode an explicit one-pass parameter (tile width / count, WL, orientation, paper mode)
     // asks for the one-pass tiles
     const bool one_pass_forced = opt.tile_width > 0 || opt.num_tiles >= 0 || opt.workload_size > 0 ||
-                                 opt.workload_sizes || opt.orient != 0 || opt.split_long_rows == 0;
+                                 opt.workload_sizes || opt.orient != 0 || opt.split_long_rows == 0 ||
+                                 opt.keep_col_order != 0;
     p->two_phase = opt.two_phase == 1;
     bool built = false;
     if (opt.two_phase == -1 && !one_pass_forced && nnz > 0 && p->two_phase_us < 1.25 * p->one_pass_us) {
@@ -434,6 +436,7 @@ __attribute__((visibility("default"))) void spmv_options_default(spmv_options* o
     o->align_rm = 8; o->split_long_rows = 1; o->camping_pad = 0; o->pattern = 0; o->ell_h = 32;
     o->stage_x = 1; o->perf_table_path = nullptr; o->orient = 0;
     o->two_phase = -1; o->pb_region = 0; o->pb_chunk = 0; o->pb_xcap = 0; o->pb_group = 0;
+    o->keep_col_order = 0;
 }
 
 __attribute__((visibility("default")))

@@ -269,17 +269,19 @@ namespace {
 struct Dist {
     int P = 1, rank = 0;
     uint8_t* d_half_local = nullptr;         // HITS: half flag per local row
-    uint8_t* d_col_half = nullptr;           // HITS: half flag per permuted column (k < nzc)
+    uint8_t* d_col_half = nullptr;           // HITS: per G position 0 / 1 = half of its vertex, 2 = no value
     int64_t n_local = 0, S = 0, slot = 0;    // owned rows, exchanged rows per slot, slot floats (S + partials)
     int64_t S_full = 0;                      // owned rows per slot of the one-time result gather
-    int64_t nzc = 0;                         // local columns with entries (plan column prefix)
+    int64_t g_floats = 0;                    // exchange buffer length (the local plan's x)
     std::vector<int64_t> gpos;               // vertex -> position in the gathered buffer (-1: never exchanged)
     std::vector<int64_t> gpos_full;          // vertex -> position in the result gather
     std::vector<int32_t> owned;              // local row -> vertex
     std::vector<int64_t> lrow;               // vertex -> local row index on its owner
     int64_t q_local = -1;
-    float* d_G = nullptr;                    // gathered buffer: P slots (needed mode: own slot + P-1 segments)
-    int32_t* d_idx = nullptr;                // x'[k] = G[idx[k]] for k < nzc
+    // exchange buffer, double buffered: iteration k reads x from d_Gb[k & 1] (the local plan's
+    // columns are G positions) while its epilogue writes the next x into d_Gb[(k + 1) & 1]'s own
+    // slot; P slots (needed mode: own slot + P-1 segments)
+    float* d_Gb[2] = {nullptr, nullptr};
     int64_t* d_part_off = nullptr;           // [P] offset of rank q's fp64 partials in d_G
     // needed-columns exchange (spmv_iter_opts.exchange = 1)
     int exchange = 0;
@@ -300,13 +302,6 @@ __global__ void dist_pack(const float* __restrict__ slot, const int32_t* __restr
 }
 
 constexpr int64_t kPartialFloats = 8;        // four fp64 partials, 16-byte multiple
-
-__global__ void dist_permute(const float* __restrict__ G, const int32_t* __restrict__ idx,
-                             float* __restrict__ xp, int64_t nzc, const tc::Ctrl* ctrl) {
-    if (*(volatile const int32_t*)&ctrl->done) return;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nzc; k += (int64_t)gridDim.x * blockDim.x)
-        xp[k] = __ldg(G + __ldg(idx + k));
-}
 
 // sum the P ranks' partials in rank order (identical on every rank: deterministic), advance
 __global__ void dist_finalize(const float* G, const int64_t* part_off, int P, tc::Ctrl* ctrl, int rwr) {
@@ -385,18 +380,26 @@ __global__ void __launch_bounds__(512) hits_dist_post(float* slot_y, float* v_ol
     if (threadIdx.x == 0) { ctrl->ticket = 0; *res_out = s[0]; }
 }
 
-__global__ void hits_dist_permute(const float* __restrict__ G, const int32_t* __restrict__ idx,
-                                  const uint8_t* __restrict__ col_half, float* __restrict__ xp, int64_t nzc,
-                                  const tc::Ctrl* ctrl) {
+// the gathered raw products normalised in place (they are the next x, read by the SpMV straight
+// from G): v = y / |y_half|, a zero half -> uniform (R5); partial and padding positions kept
+__global__ void hits_dist_scale(float* __restrict__ G, const uint8_t* __restrict__ gh, int64_t n,
+                                const tc::Ctrl* ctrl) {
     if (*(volatile const int32_t*)&ctrl->done) return;
     const double n0 = ctrl->norm[0], n1 = ctrl->norm[1];
     const float uni = (float)ctrl->uniform;
     const float s0 = n0 > 0.0 ? (float)(1.0 / n0) : 0.0f, s1 = n1 > 0.0 ? (float)(1.0 / n1) : 0.0f;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nzc; k += (int64_t)gridDim.x * blockDim.x) {
-        const int h = col_half[k];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int h = gh[k];
+        if (h == 2) continue;
         const double nn = h ? n1 : n0;
-        xp[k] = nn > 0.0 ? __ldg(G + __ldg(idx + k)) * (h ? s1 : s0) : uni;
+        G[k] = nn > 0.0 ? G[k] * (h ? s1 : s0) : uni;
     }
+}
+
+// every value position of G set to v (HITS a(0) = h(0) = 1/|V|, L440)
+__global__ void g_fill_values(float* __restrict__ G, const uint8_t* __restrict__ gh, int64_t n, float v) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        if (gh[k] != 2) G[k] = v;
 }
 
 __global__ void fill_f(float* a, int64_t n, float v) {
@@ -438,21 +441,21 @@ spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
 
 // the per-iteration exchange: one in-place allgather of equal slots, or (needed mode) the packed
 // per-peer segments by grouped point-to-point sends / receives
-spmv_status exchange(spmv_comm c, Dist* D, const tc::Ctrl* ctrl, int sm_count, cudaStream_t st) {
-    if (!D->exchange) return allgather(c, D->d_G, D->slot, st);
+spmv_status exchange(spmv_comm c, Dist* D, float* G, const tc::Ctrl* ctrl, int sm_count, cudaStream_t st) {
+    if (!D->exchange) return allgather(c, G, D->slot, st);
     if (c->world == 1) return SPMV_OK;
-    if (D->n_send) dist_pack<<<sm_count * 2, 256, 0, st>>>(D->d_G, D->d_sidx, D->d_S, D->n_send, ctrl);
+    if (D->n_send) dist_pack<<<sm_count * 2, 256, 0, st>>>(G, D->d_sidx, D->d_S, D->n_send, ctrl);
     if (c->lb) {
         // rank q's segment for us sits at q's soff[rank]; it lands at our roff[q]
         const int me = D->rank;
         return loopback_pull(c, D->d_S, D->soff.data(), [&](int, const int64_t* offs) { return offs[me]; },
-                             [&](int q) { return D->roff[q]; }, [&](int q) { return D->rcnt[q]; }, D->d_G, st);
+                             [&](int q) { return D->roff[q]; }, [&](int q) { return D->rcnt[q]; }, G, st);
     }
     spmv_status s = nccl_status(g_nccl.GroupStart(), "ncclGroupStart");
     for (int q = 0; q < D->P && !s; ++q) {
         if (q == D->rank) continue;
         s = nccl_status(g_nccl.Send(D->d_S + D->soff[q], (size_t)D->scnt[q], ncclFloat32, q, c->comm, st), "ncclSend");
-        if (!s) s = nccl_status(g_nccl.Recv(D->d_G + D->roff[q], (size_t)D->rcnt[q], ncclFloat32, q, c->comm, st), "ncclRecv");
+        if (!s) s = nccl_status(g_nccl.Recv(G + D->roff[q], (size_t)D->rcnt[q], ncclFloat32, q, c->comm, st), "ncclRecv");
     }
     spmv_status e = nccl_status(g_nccl.GroupEnd(), "ncclGroupEnd");
     return s ? s : e;
@@ -562,9 +565,18 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
             for (int64_t u = 0; u < n; ++u) col_ne[u] = len[u] != 0;
         std::vector<int64_t> cnt_ne(D->P, 0), cnt_all(D->P, 0);
         for (int64_t i = 0; i < n; ++i) { cnt_ne[owner[i]] += col_ne[i]; cnt_all[owner[i]]++; }
-        std::vector<int64_t> next_ne(D->P, 0), next_e(cnt_ne);
+        // Rank-contiguous relabel: rank q's vertices occupy slot q of the exchange buffer G, ordered
+        // by (column length desc, id asc) -- the non-empty columns first, the densest first
+        // (Solution 2, L66, inside each slot).  The local plan reads G itself as its x (columns
+        // given in G positions, keep_col_order), so no per-iteration gather builds x from G.
         D->lrow.resize(n);
-        for (int64_t i = 0; i < n; ++i) D->lrow[i] = col_ne[i] ? next_ne[owner[i]]++ : next_e[owner[i]]++;
+        {
+            std::vector<int64_t> order(n);
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return len[a] > len[b]; });
+            std::vector<int64_t> next(D->P, 0);
+            for (int64_t i : order) D->lrow[i] = next[owner[i]]++;
+        }
         const int64_t S_ex = n ? *std::max_element(cnt_ne.begin(), cnt_ne.end()) : 0;
         D->S = (S_ex + 3) / 4 * 4;
         D->slot = D->S + kPartialFloats;
@@ -578,44 +590,18 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
             if (owner[i] == D->rank) D->owned[D->lrow[i]] = (int32_t)i;
         }
         D->n_local = (int64_t)D->owned.size();
-        // local rows (lrow order: non-empty columns first, each part by ascending id), global ids
-        std::vector<int64_t> lrp(D->n_local + 1, 0);
-        for (int64_t r = 0; r < D->n_local; ++r) lrp[r + 1] = lrp[r] + row_len(D->owned[r]);
-        std::vector<int32_t> lcol(lrp[D->n_local]);
-        std::vector<char> seen(n, 0);
-        for (int64_t r = 0; r < D->n_local; ++r) {
-            const int64_t v = D->owned[r];
-            const int32_t* c = row_cols(v);
-            const int64_t L = row_len(v);
-            for (int64_t k = 0; k < L; ++k) {
-                if (c[k] < 0 || c[k] >= n) { set_error("column out of range"); throw SPMV_EINVAL; }
-                lcol[lrp[r] + k] = c[k];
-                seen[c[k]] = 1;
-            }
-        }
-        for (int64_t j = 0; j < n; ++j) D->nzc += seen[j];
-        spmv_options opt;
-        if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
-        opt.pattern = 1;
-        opt.two_phase = 0;     // the row-partitioned epilogue runs on the one-pass tiles
-        if ((st = tc::create_plan(D->n_local, n, lrp[D->n_local], lrp.data(), lcol.data(), nullptr, &opt, device, &s->plan))) throw st;
-        spmv_plan_s* p = s->plan;
-        // the plan's columns are ordered by local length: the first nzc have entries
-        std::vector<int32_t> idx(D->nzc);
+        // exchange layout: allgather slots, or (needed columns) the own slot then
+        // one segment per peer holding the values of its vertices our rows read (ascending id,
+        // padded to 4 floats) + its partials
         std::vector<int64_t> part_off(D->P);
         int64_t g_floats = (int64_t)D->P * D->slot;
         D->exchange = s->it.exchange == 1;
         if (D->exchange && li) { set_error("exchange = 1 needs the full graph on every rank"); throw SPMV_EINVAL; }
+        std::vector<std::vector<int32_t>> recv;
         if (!D->exchange) {
-            for (int64_t k = 0; k < D->nzc; ++k) {
-                idx[k] = (int32_t)D->gpos[p->perm[k]];
-                if (idx[k] < 0) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
-            }
             for (int32_t q = 0; q < D->P; ++q) part_off[q] = (int64_t)q * D->slot + D->S;
         } else {
-            // needed columns: own slot first, then one segment per peer holding the
-            // values of its vertices our rows read (ascending id, padded to 4 floats) + its partials
-            std::vector<std::vector<int32_t>> send, recv;
+            std::vector<std::vector<int32_t>> send;
             needed_lists_impl(n, mrp.data(), mcol.data(), owner.data(), D->P, D->rank, send, recv);
             D->soff.assign(D->P, 0); D->scnt.assign(D->P, 0); D->roff.assign(D->P, 0); D->rcnt.assign(D->P, 0);
             int64_t ro = D->slot, so = 0;
@@ -632,13 +618,6 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
             }
             g_floats = ro;
             D->n_send = so;
-            for (int64_t k = 0; k < D->nzc; ++k) {
-                const int32_t v = p->perm[k], q = owner[v];
-                if (q == D->rank) { idx[k] = (int32_t)D->lrow[v]; continue; }
-                auto it = std::lower_bound(recv[q].begin(), recv[q].end(), v);
-                if (it == recv[q].end() || *it != v) { set_error("internal: referenced column not received"); throw SPMV_EINVAL; }
-                idx[k] = (int32_t)(D->roff[q] + (it - recv[q].begin()));
-            }
             if (so) {
                 if ((e = cudaMalloc(&D->d_S, so * sizeof(float))) || (e = cudaMalloc(&D->d_sidx, so * sizeof(int32_t))) ||
                     (e = cudaMemcpy(D->d_sidx, sidx.data(), so * sizeof(int32_t), cudaMemcpyHostToDevice))) {
@@ -646,6 +625,39 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
                 }
             }
         }
+        D->g_floats = g_floats;
+        // G position of the value of vertex v that this rank's rows read
+        auto gcol = [&](int64_t v) -> int64_t {
+            if (!D->exchange) return D->gpos[v];
+            const int32_t q = owner[v];
+            if (q == D->rank) return D->lrow[v];
+            auto it = std::lower_bound(recv[q].begin(), recv[q].end(), (int32_t)v);
+            if (it == recv[q].end() || *it != v) return -1;
+            return D->roff[q] + (it - recv[q].begin());
+        };
+        // local rows (lrow order), columns as G positions
+        std::vector<int64_t> lrp(D->n_local + 1, 0);
+        for (int64_t r = 0; r < D->n_local; ++r) lrp[r + 1] = lrp[r] + row_len(D->owned[r]);
+        std::vector<int32_t> lcol(lrp[D->n_local]);
+        for (int64_t r = 0; r < D->n_local; ++r) {
+            const int64_t v = D->owned[r];
+            const int32_t* c = row_cols(v);
+            const int64_t L = row_len(v);
+            for (int64_t k = 0; k < L; ++k) {
+                if (c[k] < 0 || c[k] >= n) { set_error("column out of range"); throw SPMV_EINVAL; }
+                const int64_t gp = gcol(c[k]);
+                if (gp < 0) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
+                lcol[lrp[r] + k] = (int32_t)gp;
+            }
+        }
+        spmv_options opt;
+        if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
+        opt.pattern = 1;
+        opt.two_phase = 0;         // the row-partitioned epilogue runs on the one-pass tiles
+        opt.keep_col_order = 1;    // x is G itself
+        opt.num_tiles = -1; opt.tile_width = 0;
+        if ((st = tc::create_plan(D->n_local, g_floats, lrp[D->n_local], lrp.data(), lcol.data(), nullptr, &opt, device, &s->plan))) throw st;
+        spmv_plan_s* p = s->plan;
         std::vector<float> inv(std::max<int64_t>(D->n_local, 1), 0.0f);
         int64_t n_dangling = 0;
         for (int64_t u = 0; u < n; ++u) n_dangling += (len[u] == 0);
@@ -655,12 +667,12 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         }
         s->n_dangling = n_dangling;
 #define CKD(x) do { if ((e = (x)) != cudaSuccess) { st = cuda_status(e, #x); throw st; } } while (0)
-        CKD(cudaMalloc(&D->d_G, (size_t)g_floats * sizeof(float)));
-        CKD(cudaMemset(D->d_G, 0, (size_t)g_floats * sizeof(float)));
+        for (int b = 0; b < 2; ++b) {
+            CKD(cudaMalloc(&D->d_Gb[b], (size_t)g_floats * sizeof(float)));
+            CKD(cudaMemset(D->d_Gb[b], 0, (size_t)g_floats * sizeof(float)));
+        }
         CKD(cudaMalloc(&D->d_part_off, D->P * sizeof(int64_t)));
         CKD(cudaMemcpy(D->d_part_off, part_off.data(), D->P * sizeof(int64_t), cudaMemcpyHostToDevice));
-        CKD(cudaMalloc(&D->d_idx, std::max<int64_t>(D->nzc, 1) * sizeof(int32_t)));
-        if (D->nzc) CKD(cudaMemcpy(D->d_idx, idx.data(), D->nzc * sizeof(int32_t), cudaMemcpyHostToDevice));
         const int64_t nl = std::max<int64_t>(D->n_local, 1);
         CKD(cudaMalloc(&s->d_p, (nl + 4) * sizeof(float)));
         CKD(cudaMalloc(&s->d_y, (nl + 4) * sizeof(float)));
@@ -669,9 +681,13 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         CKD(cudaMalloc(&s->d_ctrl, sizeof(Ctrl)));
         CKD(cudaMemset(s->d_ctrl, 0, sizeof(Ctrl)));
         if (algo == SPMV_ALGO_HITS) {
-            std::vector<uint8_t> hl(nl, 0), ch(std::max<int64_t>(D->nzc, 1), 0);
+            // per G position: 0 authority, 1 hub (vertex >= nv), 2 no value (partials, padding)
+            std::vector<uint8_t> hl(nl, 0), ch(std::max<int64_t>(g_floats, 1), 2);
             for (int64_t r = 0; r < D->n_local; ++r) hl[r] = D->owned[r] >= nv;
-            for (int64_t k = 0; k < D->nzc; ++k) ch[k] = p->perm[k] >= nv;
+            for (int64_t v = 0; v < n; ++v) {
+                const int64_t gp = gcol(v);
+                if (gp >= 0) ch[gp] = v >= nv;
+            }
             CKD(cudaMalloc(&D->d_half_local, nl));
             CKD(cudaMemcpy(D->d_half_local, hl.data(), nl, cudaMemcpyHostToDevice));
             CKD(cudaMalloc(&D->d_col_half, ch.size()));
@@ -741,18 +757,17 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     c.tele = rwr ? 0.0 : c.c * ((double)s->n_dangling / n) / n + (1.0 - c.c) / n;
     c.uniform = s->it.hits_norm == 1 ? 1.0 / n : 1.0 / std::sqrt(n);
     if ((e = cudaMemcpyAsync(s->d_ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st))) return cuda_status(e, "ctrl");
-    float* zslot = D->exchange ? D->d_G : D->d_G + (int64_t)D->rank * D->slot;
+    // own slot of buffer b (where the epilogue writes the next x / raw product)
+    auto own = [&](int b) { return D->exchange ? D->d_Gb[b] : D->d_Gb[b] + (int64_t)D->rank * D->slot; };
     const int g = p->sm_count * 4;
     spmv_status ss = SPMV_OK;
     if (hitsa) {   // a(0) = h(0) = 1/|V| (L440): own rows and every gathered column
         fill_f<<<g, 256, 0, st>>>(s->d_p, D->n_local, (float)(1.0 / n));
-        fill_f<<<g, 256, 0, st>>>(p->d_xp, D->nzc, (float)(1.0 / n));
-        cudaMemsetAsync(zslot + D->S, 0, kPartialFloats * sizeof(float), st);
+        g_fill_values<<<g, 256, 0, st>>>(D->d_Gb[0], D->d_col_half, D->g_floats, (float)(1.0 / n));
     } else {
-        dist_init<<<g, 256, 0, st>>>(s->d_p, zslot, s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
+        dist_init<<<g, 256, 0, st>>>(s->d_p, own(0), s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
         init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
-        if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
-        dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+        if ((ss = exchange(s->comm, D, D->d_Gb[0], s->d_ctrl, p->sm_count, st))) return ss;
     }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -774,6 +789,9 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     while (true) {
         for (int b = 0; b < batch; ++b) {
             const size_t nu = s->tiles_used.size();
+            float* Gx = D->d_Gb[launched & 1];          // this iteration's x
+            float* Gn = D->d_Gb[(launched + 1) & 1];    // the next x (own slot written here, then exchanged)
+            float* zslot = own((launched + 1) & 1);
             if (hitsa) {
                 for (size_t i = 0; i < nu; ++i) {
                     EpiHitsSpmv epi{};
@@ -781,15 +799,17 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                     epi.slots = s->d_slots; epi.slot_base = s->slot_base[i]; epi.total_slots = s->total_slots;
                     epi.is_last = (i + 1 == nu); epi.l2 = s->it.hits_norm != 1;
                     epi.dist_out = reinterpret_cast<double*>(zslot + D->S);
-                    if ((e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], p->d_xp, epi, st)))
+                    if ((e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], Gx, epi, st)))
                         return cuda_status(e, "tile launch");
                 }
                 if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
-                if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
-                hits_dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->d_part_off, D->P, s->d_ctrl, s->it.hits_norm != 1);
+                if ((ss = exchange(s->comm, D, Gn, s->d_ctrl, p->sm_count, st))) return ss;
+                hits_dist_finalize<<<1, 32, 0, st>>>(Gn, D->d_part_off, D->P, s->d_ctrl, s->it.hits_norm != 1);
+                // the normalisation's L1 change travels with the NEXT exchange: it goes to the
+                // partials of the buffer the next iteration writes its product into
                 hits_dist_post<<<g, 512, 0, st>>>(zslot, s->d_p, D->d_half_local, D->n_local, s->d_ctrl, s->d_slots,
-                                                  reinterpret_cast<double*>(zslot + D->S) + 2);
-                hits_dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, D->d_col_half, p->d_xp, D->nzc, s->d_ctrl);
+                                                  reinterpret_cast<double*>(own(launched & 1) + D->S) + 2);
+                hits_dist_scale<<<g, 256, 0, st>>>(Gn, D->d_col_half, D->g_floats, s->d_ctrl);
                 mark_iter();
                 ++launched;
                 continue;
@@ -802,13 +822,12 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                 epi.total_slots = s->total_slots; epi.is_last = (i + 1 == nu); epi.cond = 0;
                 epi.rwr = rwr;
                 epi.dist_out = reinterpret_cast<double*>(zslot + D->S);
-                if ((e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], p->d_xp, epi, st)))
+                if ((e = launch_tile(*p, s->tiles_used[i], s->grids[s->tiles_used[i]], Gx, epi, st)))
                     return cuda_status(e, "tile launch");
             }
             if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
-            if ((ss = exchange(s->comm, D, s->d_ctrl, p->sm_count, st))) return ss;
-            dist_finalize<<<1, 32, 0, st>>>(D->d_G, D->d_part_off, D->P, s->d_ctrl, rwr);
-            dist_permute<<<g, 256, 0, st>>>(D->d_G, D->d_idx, p->d_xp, D->nzc, s->d_ctrl);
+            if ((ss = exchange(s->comm, D, Gn, s->d_ctrl, p->sm_count, st))) return ss;
+            dist_finalize<<<1, 32, 0, st>>>(Gn, D->d_part_off, D->P, s->d_ctrl, rwr);
             mark_iter();
             ++launched;
         }
@@ -873,7 +892,7 @@ void solver_destroy_dist(spmv_solver s) {
     Dist* D = static_cast<Dist*>(s->dist);
     cudaSetDevice(s->device);
     if (D) {
-        cudaFree(D->d_G); cudaFree(D->d_idx); cudaFree(D->d_half_local); cudaFree(D->d_col_half);
+        cudaFree(D->d_Gb[0]); cudaFree(D->d_Gb[1]); cudaFree(D->d_half_local); cudaFree(D->d_col_half);
         cudaFree(D->d_part_off); cudaFree(D->d_S); cudaFree(D->d_sidx);
         delete D;
     }

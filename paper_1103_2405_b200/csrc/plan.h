@@ -85,7 +85,7 @@ inline bool row_major(int32_t orient, int64_t w, int64_t hq) {
 void set_error(const std::string& msg);
 
 spmv_status prepare(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
-                    const int32_t* col, const float* val, bool pattern, Prepared& P);
+                    const int32_t* col, const float* val, bool pattern, Prepared& P, bool keep_order = false);
 int32_t paper_tile_count(const Prepared& P, int64_t tile_width);
 // Sorted (descending) in-tile row-length histogram of every tile for a given tiling:
 // hist[t] = vector of (length, count) pairs, lengths descending; zero rows go to the remainder.

@@ -341,8 +341,10 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
         std::vector<int32_t> Ts;
         if (opt.num_tiles >= 0) Ts.push_back((int32_t)std::min<int64_t>(opt.num_tiles, max_tiles));
         else {
-            // Alg. 1 gives the upper bound; the model picks the count (B200 terms included)
-            const int32_t Tp = std::min<int32_t>(paper_tile_count(P, tw), 16);
+            // Alg. 1 gives the upper bound; the model picks the count (B200 terms included).
+            // Columns in the caller's order (keep_col_order) are not length-sorted: no dense
+            // tiles, only the L2-sized ones below
+            const int32_t Tp = opt.keep_col_order ? 0 : std::min<int32_t>(paper_tile_count(P, tw), 16);
             for (int32_t T = 0; T <= Tp; T = (T < 4 ? T + 1 : T * 2)) Ts.push_back(T);
             if (Ts.back() != Tp) Ts.push_back(Tp);
         }

@@ -248,3 +248,17 @@ def test_parallel_transpose_equals_serial(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
+
+
+def test_keep_col_order_layout():
+    """keep_col_order: the columns keep the caller's order (perm = identity, no dense tiles) and the
+    layout still decodes to the input entries."""
+    from paper_1103_2405_b200 import Plan
+    rp, col, val = graphgen.random_csr(500, 700, 9000, seed=3, kind="powerlaw", valued=True)
+    p = Plan(500, 700, rp, col, val, device=-1, keep_col_order=1)
+    lay = p.layout()
+    assert np.array_equal(lay["perm"], np.arange(700))
+    assert p.stats()["num_tiles"] == 0
+    r, c, v = p.to_coo()
+    assert sorted(zip(r.tolist(), c.tolist(), v.tolist())) == sorted(
+        zip(np.repeat(np.arange(500), np.diff(rp)).tolist(), col.tolist(), val.tolist()))

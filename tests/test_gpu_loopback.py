@@ -82,6 +82,10 @@ def test_pagerank_loopback(P, exchange, gpu):
     ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
     assert np.abs(p.astype(np.float64) - ref).sum() < 1e-6, info
     assert info["converged"]
+    # the stop rule agrees with the single-GPU solver on the same (one-pass) kernels
+    from paper_1103_2405_b200 import Solver
+    s1 = Solver("pagerank", G.n, G.row_ptr, G.col, device=0, two_phase=0)
+    assert abs(s1.run()["iterations"] - info["iterations"]) <= 1
 
 
 @pytest.mark.parametrize("P", [2, 3, 8])
@@ -107,6 +111,10 @@ def test_hits_loopback(P, norm, exchange, gpu):
     bar_a = 1e-6 * (1.0 if norm == 1 else np.abs(ra).sum())
     bar_h = 1e-6 * (1.0 if norm == 1 else np.abs(rh).sum())
     assert np.abs(a - ra).sum() < bar_a and np.abs(h - rh).sum() < bar_h, info
+    if norm == 1:   # sum-1 halves converge cleanly: the stop rule agrees with one GPU
+        from paper_1103_2405_b200 import Solver
+        s1 = Solver("hits", G.n, G.row_ptr, G.col, device=0, two_phase=0, iter_kw=dict(hits_norm=1))
+        assert abs(s1.run()["iterations"] - info["iterations"]) <= 1
 
 
 def test_pagerank_loopback_mid_graph(gpu):
