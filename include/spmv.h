@@ -221,6 +221,10 @@ typedef struct {
     double ms_total;       /* device time of the iteration loop (CUDA events) */
     double us_per_iter;
     double predicted_us_per_iter;
+    double phase_us[3];    /* row-partitioned solvers: mean per iteration of the local SpMV (with
+                            * its fused epilogue), the exchange, and the rest (partial sums, HITS
+                            * normalisation), from CUDA events between the phases; single GPU:
+                            * {us_per_iter, 0, 0} */
 } spmv_iter_result;
 
 /* Graph input for all three: adjacency A of G = (V,E), CSR with row u listing the targets v of

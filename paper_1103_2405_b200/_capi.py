@@ -59,7 +59,8 @@ class IterOpts(ctypes.Structure):
 
 class IterResult(ctypes.Structure):
     _fields_ = [("iterations", c_i32), ("converged", c_i32), ("residual", c_f64),
-                ("ms_total", c_f64), ("us_per_iter", c_f64), ("predicted_us_per_iter", c_f64)]
+                ("ms_total", c_f64), ("us_per_iter", c_f64), ("predicted_us_per_iter", c_f64),
+                ("phase_us", c_f64 * 3)]
 
 
 # every exported symbol declared in include/spmv.h, with its signature

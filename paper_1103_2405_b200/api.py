@@ -246,7 +246,7 @@ class Solver:
             check(st, "spmv_solver_run")
         return dict(iterations=r.iterations, converged=bool(r.converged), residual=r.residual,
                     ms_total=r.ms_total, us_per_iter=r.us_per_iter,
-                    predicted_us_per_iter=r.predicted_us_per_iter)
+                    predicted_us_per_iter=r.predicted_us_per_iter, phase_us=list(r.phase_us))
 
     def run_batch(self, queries, stream=None) -> dict:
         """Batched RWR: all queries (<= 32) iterate together (spmv_solver_run_batch)."""

@@ -532,6 +532,7 @@ spmv_status spmv_solver_run_batch(spmv_solver s, const int64_t* queries, int32_t
         res->iterations = c.iter; res->residual = c.residual;
         res->converged = s->it.fixed_iters > 0 ? 1 : (c.residual < s->it.tol);
         res->ms_total = ms; res->us_per_iter = c.iter ? 1000.0 * ms / c.iter : 0.0;
+        res->phase_us[0] = res->us_per_iter; res->phase_us[1] = res->phase_us[2] = 0.0;
         res->predicted_us_per_iter = p->predicted_us;
     }
     if (s->it.fixed_iters <= 0 && !(c.residual < s->it.tol)) { set_error("max_iter reached"); return SPMV_ENOCONV; }

@@ -769,11 +769,12 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
         init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
         if ((ss = exchange(s->comm, D, D->d_Gb[0], s->d_ctrl, p->sm_count, st))) return ss;
     }
+    // host allocations before the first event: the GPU must not idle inside the timed region
+    Ctrl* hc = nullptr;
+    cudaMallocHost(&hc, sizeof(Ctrl));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
-    Ctrl* hc = nullptr;
-    cudaMallocHost(&hc, sizeof(Ctrl));
     const int batch = 8;
     const int cap = std::max(s->it.max_iter, s->it.fixed_iters) + batch;
     int launched = 0;
@@ -785,6 +786,14 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
         cudaEventCreate(&v);
         cudaEventRecord(v, st);
         ev_it.push_back(v);
+    };
+    // phase boundaries of each iteration: after the local SpMV, after the exchange
+    std::vector<cudaEvent_t> ev_spmv, ev_exch;
+    auto mark = [&](std::vector<cudaEvent_t>& v) {
+        cudaEvent_t x;
+        cudaEventCreate(&x);
+        cudaEventRecord(x, st);
+        v.push_back(x);
     };
     while (true) {
         for (int b = 0; b < batch; ++b) {
@@ -803,7 +812,9 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                         return cuda_status(e, "tile launch");
                 }
                 if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
+                mark(ev_spmv);
                 if ((ss = exchange(s->comm, D, Gn, s->d_ctrl, p->sm_count, st))) return ss;
+                mark(ev_exch);
                 hits_dist_finalize<<<1, 32, 0, st>>>(Gn, D->d_part_off, D->P, s->d_ctrl, s->it.hits_norm != 1);
                 // the normalisation's L1 change travels with the NEXT exchange: it goes to the
                 // partials of the buffer the next iteration writes its product into
@@ -826,7 +837,9 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                     return cuda_status(e, "tile launch");
             }
             if (nu == 0) cudaMemsetAsync(zslot + D->S, 0, 2 * sizeof(double), st);
+            mark(ev_spmv);
             if ((ss = exchange(s->comm, D, Gn, s->d_ctrl, p->sm_count, st))) return ss;
+            mark(ev_exch);
             dist_finalize<<<1, 32, 0, st>>>(Gn, D->d_part_off, D->P, s->d_ctrl, rwr);
             mark_iter();
             ++launched;
@@ -848,8 +861,18 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     last = std::min<int64_t>(std::max<int64_t>(last, 0), (int64_t)ev_it.size() - 1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, last >= 0 ? ev_it[last] : e1);
+    double ph[3] = {0.0, 0.0, 0.0};
+    for (int64_t i = 0; i <= last; ++i) {
+        float a = 0.f, b = 0.f, c3 = 0.f;
+        cudaEventElapsedTime(&a, i ? ev_it[i - 1] : e0, ev_spmv[i]);
+        cudaEventElapsedTime(&b, ev_spmv[i], ev_exch[i]);
+        cudaEventElapsedTime(&c3, ev_exch[i], ev_it[i]);
+        ph[0] += a; ph[1] += b; ph[2] += c3;
+    }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     for (auto v : ev_it) cudaEventDestroy(v);
+    for (auto v : ev_spmv) cudaEventDestroy(v);
+    for (auto v : ev_exch) cudaEventDestroy(v);
     cudaFreeHost(hc);
     s->last = c;
     if (res) {
@@ -857,6 +880,7 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
         res->converged = s->it.fixed_iters > 0 ? 1 : (c.residual < s->it.tol);
         res->ms_total = ms; res->us_per_iter = c.iter ? 1000.0 * ms / c.iter : 0.0;
         res->predicted_us_per_iter = p->predicted_us;
+        for (int k = 0; k < 3; ++k) res->phase_us[k] = last >= 0 ? 1000.0 * ph[k] / (double)(last + 1) : 0.0;
     }
     if (s->it.fixed_iters <= 0 && !(c.residual < s->it.tol)) { set_error("max_iter reached"); return SPMV_ENOCONV; }
     return SPMV_OK;

@@ -185,12 +185,10 @@ static cudaError_t enqueue_iteration(spmv_solver_s* s, int parity, cudaStream_t 
 
 // the iteration loop without a graph: iterations (double-buffered z) enqueued in batches of 8,
 // the stop flag read after each batch; *stop = the event after the iteration that stopped
-static cudaError_t run_host_loop(spmv_solver_s* s, cudaStream_t st, cudaEvent_t* stop) {
+static cudaError_t run_host_loop(spmv_solver_s* s, cudaStream_t st, cudaEvent_t* stop, Ctrl* hc) {
     const int batch = 8;
     const int cap = std::max(s->it.max_iter, s->it.fixed_iters) + batch;
-    Ctrl* hc = nullptr;
-    cudaError_t e = cudaMallocHost(&hc, sizeof(Ctrl));
-    if (e) return e;
+    cudaError_t e = cudaSuccess;
     std::vector<cudaEvent_t> ev;
     int launched = 0;
     while (!e) {
@@ -212,7 +210,6 @@ static cudaError_t run_host_loop(spmv_solver_s* s, cudaStream_t st, cudaEvent_t*
         ev[last] = nullptr;
     }
     for (auto v : ev) if (v) cudaEventDestroy(v);
-    cudaFreeHost(hc);
     return e;
 }
 
@@ -342,12 +339,15 @@ spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_ite
                                         s->algo == SPMV_ALGO_RWR, (int32_t)c.q, (float)(1.0 / n));
     }
     if ((e = cudaGetLastError())) return cuda_status(e, "init");
+    Ctrl* hc = nullptr;                       // pinned, allocated before the timed region
+    if (s->it.host_loop && (e = cudaMallocHost(&hc, sizeof(Ctrl)))) return cuda_status(e, "cudaMallocHost");
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
     cudaEvent_t e_stop = nullptr;
-    if (s->it.host_loop) e = run_host_loop(s, st, &e_stop);   // the same kernels, host-enqueued
+    if (s->it.host_loop) e = run_host_loop(s, st, &e_stop, hc);   // the same kernels, host-enqueued
     else e = cudaGraphLaunch(s->exec, st);
+    if (hc) cudaFreeHost(hc);
     cudaEventRecord(e1, st);
     if (e) {
         cudaEventDestroy(e0); cudaEventDestroy(e1);
@@ -370,6 +370,7 @@ spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_ite
         res->converged = s->it.fixed_iters > 0 ? 1 : (c.residual < s->it.tol);
         res->ms_total = ms; res->us_per_iter = c.iter ? 1000.0 * ms / c.iter : 0.0;
         res->predicted_us_per_iter = s->plan->predicted_us;
+        res->phase_us[0] = res->us_per_iter; res->phase_us[1] = res->phase_us[2] = 0.0;
     }
     if (s->it.fixed_iters <= 0 && !(c.residual < s->it.tol)) { set_error("max_iter reached"); return SPMV_ENOCONV; }
     return SPMV_OK;
