@@ -185,6 +185,12 @@ spmv_status spmv_plan_layout(spmv_plan plan, spmv_layout_view* out);
  * (valued plans only), split i32[n_split*3].  Errors: EINVAL (null), ENOMEM (file not writable),
  * ECUDA (layout download). */
 spmv_status spmv_plan_export(spmv_plan plan, const char* path);
+/* Read a file written by spmv_plan_export back into a plan and upload it to `device` (-1: host
+ * only) -- a checkpoint of the preprocessing (sort, tiling, packing: paid once per matrix, L98).
+ * The tiling, WLs and layout are the file's; per-tile predictions are not stored (0).  Two-phase
+ * plans have no Format v1 file.  Errors: EINVAL (unreadable / not Format v1 / truncated), ENOMEM,
+ * ECUDA. */
+spmv_status spmv_plan_import(const char* path, int device, spmv_plan* out);
 /* Decode the layout back to COO (original row / column ids), padding dropped; arrays of nnz. */
 spmv_status spmv_plan_to_coo(spmv_plan plan, int32_t* rows, int32_t* cols, float* vals);
 /* Diagnostic (two-phase plans): one product with a per-item timeline.  trace_host receives

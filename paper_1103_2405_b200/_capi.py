@@ -78,6 +78,7 @@ SIGNATURES = {
     "spmv_plan_layout": (c_i32, [c_vp, ctypes.POINTER(LayoutView)]),
     "spmv_plan_to_coo": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "spmv_plan_export": (c_i32, [c_vp, ctypes.c_char_p]),
+    "spmv_plan_import": (c_i32, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(c_vp)]),
     "spmv_needed_lists": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "spmv_plan_launches": (c_i32, [c_vp]),
     "spmv_pb_trace": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64]),

@@ -181,6 +181,18 @@ class Plan:
         """spmv_plan_export: the layout arrays as one binary file (include/spmv.h)."""
         check(C.lib().spmv_plan_export(self._h, str(path).encode()), "spmv_plan_export")
 
+    @classmethod
+    def load(cls, path: str, device=0):
+        """spmv_plan_import: a plan from a file written by export() (preprocessing checkpoint)."""
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        check(C.lib().spmv_plan_import(str(path).encode(), int(device), ctypes.byref(h)), "spmv_plan_import")
+        self._h = h
+        self.device = device
+        s = self.stats()
+        self.n_rows, self.n_cols, self.nnz = s["n_rows"], s["n_cols"], s["nnz"]
+        return self
+
     def to_coo(self):
         r = np.zeros(max(self.nnz, 1), np.int32)
         c = np.zeros(max(self.nnz, 1), np.int32)

@@ -10,6 +10,7 @@
 
 #include "launch.cuh"
 #include "pb_launch.cuh"
+#include "trace.h"
 #include "tune.h"
 
 namespace tc {
@@ -182,6 +183,39 @@ static spmv_status create_two_phase(spmv_plan_s* p, const Prepared& P, const int
     return SPMV_OK;
 }
 
+// Upload a one-pass plan's host layout to p->device (plan creation and spmv_plan_import); on
+// failure the plan is freed.
+static spmv_status upload_one_pass(spmv_plan_s* p) {
+    cudaError_t e;
+    int64_t& b = p->device_bytes;
+    if (const char* h = std::getenv("TCSPMV_PERMUTE")) p->permute_gather = std::string(h) != "scatter";
+    if ((e = upload(&p->d_desc, p->L.desc, b)) || (e = upload(&p->d_row_id, p->L.row_id, b)) ||
+        (e = upload(&p->d_col, p->L.slot_col, b)) || (e = upload(&p->d_perm, p->perm, b)) ||
+        (!p->permute_gather && (e = upload(&p->d_inv, inverse(p->perm), b))) ||
+        (e = upload(&p->d_split, p->L.split, b))) {
+        free_device(p); delete p; return cuda_status(e, "plan upload");
+    }
+    if (!p->pattern && (e = upload(&p->d_val, p->L.slot_val, b))) {
+        free_device(p); delete p; return cuda_status(e, "plan upload");
+    }
+    std::vector<float> zf(std::max<int64_t>(p->n_chunks, 1), 0.0f);
+    std::vector<int32_t> zi(std::max<int64_t>(p->n_split, 1), 0);
+    std::vector<float> xpz(p->n_cols + 4, 0.0f);
+    std::vector<uint32_t> zs((size_t)(tc::kDynQ + 1) * (p->num_tiles + 1), 0u);
+    if ((e = upload(&p->d_partials, zf, b)) || (e = upload(&p->d_counters, zi, b)) ||
+        (e = upload(&p->d_sched, zs, b)) ||
+        (e = upload(&p->d_xp, xpz, b))) {
+        free_device(p); delete p; return cuda_status(e, "plan upload");
+    }
+    if ((e = setup_grids<EpiStore>(*p, p->grid_tile))) {
+        free_device(p); delete p; return cuda_status(e, "occupancy");
+    }
+    // release the host copy (fetched back on demand by spmv_plan_layout / to_coo)
+    p->L.desc = {}; p->L.row_id = {}; p->L.slot_col = {}; p->L.slot_val = {}; p->L.split = {};
+    p->host_valid = false;
+    return SPMV_OK;
+}
+
 // build the plan (host) and upload it; shared by spmv_plan_create and the solvers
 spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col, const float* val, const spmv_options* opt_in,
@@ -202,6 +236,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
         if ((e = cudaSetDevice(device))) return cuda_status(e, "cudaSetDevice");
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device);
     }
+    Range r_build("spmv_plan_create");
     Prepared P;
     if (opt.keep_col_order && opt.two_phase == 1) { set_error("keep_col_order is a one-pass option"); return SPMV_EINVAL; }
     spmv_status st = prepare(n_rows, n_cols, nnz, row_ptr, col, val, opt.pattern != 0, P, opt.keep_col_order != 0);
@@ -209,7 +244,10 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     BuildParams bp;
     std::vector<double> pred;
     int32_t table_loaded = 0;
-    st = choose_params(P, opt, sm_count, bp, pred, &table_loaded);
+    {
+        Range r("tune (Alg. 1-3)");
+        st = choose_params(P, opt, sm_count, bp, pred, &table_loaded);
+    }
     if (st) return st;
     if (opt.two_phase < -1 || opt.two_phase > 1) { set_error("two_phase must be -1, 0 or 1"); return SPMV_EINVAL; }
     spmv_plan_s* p = new spmv_plan_s();
@@ -241,7 +279,10 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
         if (!st) *out = p;
         return st;
     }
-    st = pack_layout(P, bp, p->L);
+    {
+        Range r("pack_layout");
+        st = pack_layout(P, bp, p->L);
+    }
     if (st) { delete p; return st; }
     p->perm = std::move(P.perm);
     p->host_valid = true;
@@ -256,35 +297,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     for (int32_t t = 0; t < p->num_tiles; ++t)
         p->tiles[t].staged = (opt.stage_x != 0) && (p->tiles[t].col_hi - p->tiles[t].col_lo) * 4 <= 227 * 1024 &&
                              (p->tiles[t].col_lo % 4 == 0);
-    if (device >= 0) {
-        cudaError_t e;
-        int64_t& b = p->device_bytes;
-        if (const char* h = std::getenv("TCSPMV_PERMUTE")) p->permute_gather = std::string(h) != "scatter";
-        if ((e = upload(&p->d_desc, p->L.desc, b)) || (e = upload(&p->d_row_id, p->L.row_id, b)) ||
-            (e = upload(&p->d_col, p->L.slot_col, b)) || (e = upload(&p->d_perm, p->perm, b)) ||
-            (!p->permute_gather && (e = upload(&p->d_inv, inverse(p->perm), b))) ||
-            (e = upload(&p->d_split, p->L.split, b))) {
-            free_device(p); delete p; return cuda_status(e, "plan upload");
-        }
-        if (!p->pattern && (e = upload(&p->d_val, p->L.slot_val, b))) {
-            free_device(p); delete p; return cuda_status(e, "plan upload");
-        }
-        std::vector<float> zf(std::max<int64_t>(p->n_chunks, 1), 0.0f);
-        std::vector<int32_t> zi(std::max<int64_t>(p->n_split, 1), 0);
-        std::vector<float> xpz(p->n_cols + 4, 0.0f);
-        std::vector<uint32_t> zs((size_t)(tc::kDynQ + 1) * (p->num_tiles + 1), 0u);
-        if ((e = upload(&p->d_partials, zf, b)) || (e = upload(&p->d_counters, zi, b)) ||
-            (e = upload(&p->d_sched, zs, b)) ||
-            (e = upload(&p->d_xp, xpz, b))) {
-            free_device(p); delete p; return cuda_status(e, "plan upload");
-        }
-        if ((e = setup_grids<EpiStore>(*p, p->grid_tile))) {
-            free_device(p); delete p; return cuda_status(e, "occupancy");
-        }
-        // release the host copy (fetched back on demand by spmv_plan_layout / to_coo)
-        p->L.desc = {}; p->L.row_id = {}; p->L.slot_col = {}; p->L.slot_val = {}; p->L.split = {};
-        p->host_valid = false;
-    }
+    if (device >= 0 && (st = upload_one_pass(p))) return st;
     p->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     *out = p;
     return SPMV_OK;
@@ -414,6 +427,7 @@ static const float* pb_x(spmv_plan_s* p, const float* x, cudaStream_t st, cudaEr
 }
 
 spmv_status execute_permuted(spmv_plan_s* p, const float* xp, float* y, cudaStream_t st) {
+    Range r("spmv_execute");
     if (p->two_phase) {
         cudaError_t e;
         xp = pb_x(p, xp, st, e);
@@ -709,6 +723,92 @@ spmv_status spmv_plan_export(spmv_plan p, const char* path) {
     put(v.split, 12 * (size_t)v.n_split);
     if (std::fclose(f) != 0) ok = false;
     if (!ok) { set_error(std::string("short write to ") + path); return SPMV_ENOMEM; }
+    return SPMV_OK;
+}
+
+// Read a Format v1 file written by spmv_plan_export and upload it (plan checkpoint / resume,
+// the sort and packing are preprocessing, paid once per matrix).
+__attribute__((visibility("default")))
+spmv_status spmv_plan_import(const char* path, int device, spmv_plan* out) {
+    if (!path || !out) { set_error("null argument"); return SPMV_EINVAL; }
+    *out = nullptr;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) { set_error(std::string("cannot open ") + path); return SPMV_EINVAL; }
+    bool ok = true;
+    auto get = [&](void* a, size_t bytes) { if (bytes && ok) ok = std::fread(a, 1, bytes, f) == bytes; };
+    char magic[8] = {0};
+    int64_t hdr[8] = {0};
+    get(magic, 8); get(hdr, sizeof(hdr));
+    if (!ok || std::memcmp(magic, "TCSPMV1", 8) != 0) { std::fclose(f); set_error("not a Format v1 plan file"); return SPMV_EINVAL; }
+    const int64_t n_rows = hdr[0], n_cols = hdr[1], nw = hdr[2], ne = hdr[3], ns = hdr[4], nsp = hdr[5], nt = hdr[6];
+    const bool valued = hdr[7] != 0;
+    if (n_rows < 0 || n_cols < 0 || nw < 0 || ne < 0 || ns < 0 || nsp < 0 || nt < 1 || nt > 64) {
+        std::fclose(f); set_error("plan file header out of range"); return SPMV_EINVAL;
+    }
+    spmv_plan_s* p = nullptr;
+    try {
+        p = new spmv_plan_s();
+        p->n_rows = n_rows; p->n_cols = n_cols; p->pattern = !valued; p->device = device;
+        spmv_options_default(&p->opt);
+        p->opt.pattern = p->pattern ? 1 : 0;
+        p->perm.resize(n_cols); get(p->perm.data(), 4 * (size_t)n_cols);
+        std::vector<int64_t> tiles(4 * nt); get(tiles.data(), 32 * (size_t)nt);
+        std::vector<int64_t> off(nw); std::vector<int32_t> rb(nw), w(nw), h(nw), sid(nw), ch(nw);
+        std::vector<uint8_t> kind(nw), kvec(nw);
+        get(off.data(), 8 * nw); get(rb.data(), 4 * nw); get(w.data(), 4 * nw); get(h.data(), 4 * nw);
+        get(sid.data(), 4 * nw); get(ch.data(), 4 * nw); get(kind.data(), nw); get(kvec.data(), nw);
+        HostLayout& L = p->L;
+        L.row_id.resize(ne); get(L.row_id.data(), 4 * (size_t)ne);
+        L.slot_col.resize(ns); get(L.slot_col.data(), 4 * (size_t)ns);
+        if (valued) { L.slot_val.resize(ns); get(L.slot_val.data(), 4 * (size_t)ns); }
+        L.split.resize(3 * nsp); get(L.split.data(), 12 * (size_t)nsp);
+        std::fclose(f); f = nullptr;
+        if (!ok) { delete p; set_error("short plan file"); return SPMV_EINVAL; }
+        L.desc.resize(nw);
+        for (int64_t j = 0; j < nw; ++j) {
+            WlDesc& d = L.desc[j];
+            d.off = off[j]; d.row_base = rb[j]; d.w = w[j]; d.h = h[j]; d.kind = kind[j]; d.kvec = kvec[j];
+            d.pad_ = 0; d.split_id = sid[j]; d.chunk = ch[j];
+        }
+        p->num_tiles = (int32_t)(nt - 1);
+        p->tiles.resize(nt);
+        int64_t nnz = 0;
+        for (int64_t t = 0; t < nt; ++t) {
+            TileInfo& ti = p->tiles[t];
+            ti.col_lo = tiles[4 * t]; ti.col_hi = tiles[4 * t + 1]; ti.wl_begin = tiles[4 * t + 2]; ti.wl_end = tiles[4 * t + 3];
+            const int32_t sent = (int32_t)(ti.col_hi - ti.col_lo);
+            for (int64_t j = ti.wl_begin; j < ti.wl_end; ++j) {
+                const WlDesc& d = L.desc[j];
+                const int64_t span = (int64_t)d.w * d.h;
+                for (int64_t k = 0; k < span; ++k) ti.nnz += L.slot_col[d.off + k] != sent;
+            }
+            nnz += ti.nnz;
+            if (t < nt - 1)
+                ti.staged = (ti.col_hi - ti.col_lo) * 4 <= 227 * 1024 && ti.col_lo % 4 == 0;
+        }
+        p->tile_width = nt > 1 ? (int32_t)(p->tiles[0].col_hi - p->tiles[0].col_lo) : (int32_t)std::min<int64_t>(n_cols, INT32_MAX);
+        p->nnz = nnz;
+        p->n_workloads = nw; p->n_slots = ns; p->n_row_entries = ne; p->n_split = nsp;
+        int64_t nch = 0;
+        for (int64_t i = 0; i < nsp; ++i) nch = std::max<int64_t>(nch, (int64_t)L.split[3 * i + 2] + L.split[3 * i + 1]);
+        p->n_chunks = L.n_chunks = nch;
+        p->host_valid = true;
+        if (device >= 0) {
+            int ndev = 0;
+            cudaError_t e = cudaGetDeviceCount(&ndev);
+            if (e != cudaSuccess || ndev == 0) { delete p; set_error("no CUDA device"); return SPMV_ECUDA; }
+            if (device >= ndev) { delete p; set_error("device ordinal out of range"); return SPMV_EINVAL; }
+            if ((e = cudaSetDevice(device))) { delete p; return cuda_status(e, "cudaSetDevice"); }
+            cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device);
+            spmv_status st = upload_one_pass(p);
+            if (st) return st;
+        }
+    } catch (const std::bad_alloc&) {
+        if (f) std::fclose(f);
+        delete p;
+        set_error("host allocation failed"); return SPMV_ENOMEM;
+    }
+    *out = p;
     return SPMV_OK;
 }
 

@@ -4,7 +4,10 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
+#include <string>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -15,6 +18,7 @@
 #include "graph_build.h"
 #include "launch.cuh"
 #include "solver.h"
+#include "trace.h"
 
 using namespace tc;
 
@@ -34,6 +38,8 @@ struct Nccl {
     int (*Recv)(void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
+    int (*CommGetAsyncError)(NcclComm, int*) = nullptr;
+    int (*CommAbort)(NcclComm) = nullptr;
     const char* (*GetErrorString)(int) = nullptr;
     bool load() {
         if (h) return true;
@@ -53,6 +59,8 @@ struct Nccl {
         Recv = (decltype(Recv))dlsym(h, "ncclRecv");
         GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
         GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
+        CommGetAsyncError = (decltype(CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+        CommAbort = (decltype(CommAbort))dlsym(h, "ncclCommAbort");
         return GetUniqueId && CommInitRank && CommDestroy && AllGather && AllReduce && Send && Recv &&
                GroupStart && GroupEnd;
     }
@@ -430,6 +438,34 @@ spmv_status loopback_pull(spmv_comm c, const void* mine, const int64_t* my_offs,
     return cuda_status(e, "loopback exchange");
 }
 
+// Failure detection: wait for the stream while polling NCCL's asynchronous error
+// state; a peer failure or a hang past the watchdog aborts the communicator (the collective
+// kernels would otherwise spin forever) and returns SPMV_ENCCL instead of blocking.
+constexpr double kWatchdogSeconds = 600.0;
+spmv_status wait_stream(spmv_comm c, cudaStream_t st, const char* what) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) return SPMV_OK;
+        if (q != cudaErrorNotReady) return cuda_status(q, what);
+        if (c && c->comm) {
+            int ae = 0;
+            if (g_nccl.CommGetAsyncError && g_nccl.CommGetAsyncError(c->comm, &ae) == 0 && ae != 0) {
+                if (g_nccl.CommAbort) g_nccl.CommAbort(c->comm);
+                c->comm = nullptr;
+                return nccl_status(ae, "NCCL asynchronous error (communicator aborted)");
+            }
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > kWatchdogSeconds) {
+            if (c && c->comm && g_nccl.CommAbort) { g_nccl.CommAbort(c->comm); c->comm = nullptr; }
+            set_error(std::string(what) + ": watchdog (" + std::to_string((int)kWatchdogSeconds) + " s) expired");
+            return c && c->world > 1 ? SPMV_ENCCL : SPMV_ECUDA;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+}
+
 spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
     if (c->world == 1) return SPMV_OK;
     if (c->lb)
@@ -442,6 +478,7 @@ spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
 // the per-iteration exchange: one in-place allgather of equal slots, or (needed mode) the packed
 // per-peer segments by grouped point-to-point sends / receives
 spmv_status exchange(spmv_comm c, Dist* D, float* G, const tc::Ctrl* ctrl, int sm_count, cudaStream_t st) {
+    tc::Range r("exchange");
     if (!D->exchange) return allgather(c, G, D->slot, st);
     if (c->world == 1) return SPMV_OK;
     if (D->n_send) dist_pack<<<sm_count * 2, 256, 0, st>>>(G, D->d_sidx, D->d_S, D->n_send, ctrl);
@@ -735,6 +772,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
 }
 
 spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res) {
+    tc::Range r_run("spmv_solver_run (row-partitioned)");
     Dist* D = static_cast<Dist*>(s->dist);
     spmv_plan_s* p = s->plan;
     if (s->algo == SPMV_ALGO_RWR && (query < 0 || query >= s->n)) { set_error("query out of range"); return SPMV_ERANGE; }
@@ -845,10 +883,12 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
             ++launched;
         }
         cudaMemcpyAsync(hc, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
-        if ((e = cudaStreamSynchronize(st))) {
+        if ((ss = wait_stream(s->comm, st, "iteration loop"))) {
             cudaFreeHost(hc);
             for (auto v : ev_it) cudaEventDestroy(v);
-            return cuda_status(e, "iteration loop");
+            for (auto v : ev_spmv) cudaEventDestroy(v);
+            for (auto v : ev_exch) cudaEventDestroy(v);
+            return ss;
         }
         if (hc->done || launched > cap) break;
     }

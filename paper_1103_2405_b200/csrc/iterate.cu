@@ -28,6 +28,7 @@
 #include "launch.cuh"
 #include "pb_launch.cuh"
 #include "solver.h"
+#include "trace.h"
 
 namespace tc {
 
@@ -42,6 +43,7 @@ using namespace tc;
 // ------------------------------------------------------------------ solver object
 static spmv_status build_solver(spmv_solver_s* s, const int64_t* row_ptr, const int32_t* col,
                                 const spmv_options* opt_in) {
+    Range r_build("spmv_solver_create");
     const int64_t n = s->n;
     std::vector<int64_t> arp; std::vector<int32_t> acol;
     clean_adjacency(n, row_ptr, col, arp, acol);
@@ -309,6 +311,7 @@ __attribute__((visibility("default")))
 spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_iter_result* res) {
     if (!s) { set_error("null solver"); return SPMV_EINVAL; }
     if (s->comm) return solver_run_dist(s, query, stream, res);
+    Range r_run("spmv_solver_run");
     if (s->algo == SPMV_ALGO_RWR && (query < 0 || query >= s->n)) { set_error("query out of range"); return SPMV_ERANGE; }
     cudaError_t e = cudaSetDevice(s->device);
     if (e) return cuda_status(e, "cudaSetDevice");

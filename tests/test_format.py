@@ -262,3 +262,33 @@ def test_keep_col_order_layout():
     r, c, v = p.to_coo()
     assert sorted(zip(r.tolist(), c.tolist(), v.tolist())) == sorted(
         zip(np.repeat(np.arange(500), np.diff(rp)).tolist(), col.tolist(), val.tolist()))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_plan_import_roundtrip(seed, tmp_path):
+    """spmv_plan_import reads back what spmv_plan_export wrote: re-exported byte for byte (every
+    layout array), the same COO decode (host-only plans)."""
+    from paper_1103_2405_b200 import Plan
+    rng = np.random.default_rng(40 + seed)
+    rp, col, val = graphgen.random_csr(400, 600, 8000, seed=seed, kind="powerlaw", valued=seed != 1)
+    p = Plan(400, 600, rp, col, val, device=-1, tile_width=64, num_tiles=int(rng.integers(0, 4)),
+             workload_size=int(rng.integers(16, 300)), two_phase=0)
+    f = tmp_path / "plan.bin"
+    p.export(f)
+    q = Plan.load(f, device=-1)
+    f2 = tmp_path / "plan2.bin"
+    q.export(f2)
+    assert f.read_bytes() == f2.read_bytes()
+    assert q.stats()["nnz"] == len(col)
+    r1, c1, v1 = p.to_coo()
+    r2, c2, v2 = q.to_coo()
+    assert sorted(zip(r1.tolist(), c1.tolist(), v1.tolist())) == sorted(zip(r2.tolist(), c2.tolist(), v2.tolist()))
+
+
+def test_plan_import_rejects_garbage(tmp_path):
+    from paper_1103_2405_b200 import Plan
+    from paper_1103_2405_b200._capi import SpmvError
+    f = tmp_path / "x.bin"
+    f.write_bytes(b"not a plan at all")
+    with pytest.raises(SpmvError):
+        Plan.load(f, device=-1)
