@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip PageRank/HITS/RWR and cpu_baseline")
+    ap.add_argument("--no-c4", action="store_true", help="skip the c4 PageRank leg (about 5 minutes)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -294,7 +295,7 @@ def main():
                 if r.get("probe") == "gather" and r.get("dist") == "skew" and r.get("mode") == 0:
                     if best is None or abs(np.log(r["S"] / G.n)) < abs(np.log(best["S"] / G.n)):
                         best = r
-        if best is not None and launch_nnz[dom] > 0:
+        if best is not None and launch_nnz[dom] > 0 and not st["two_phase"]:
             g_ach = launch_nnz[dom] / (per[dom] * 1e-3) / 1e9
             roofline["gather"] = {"achieved_G_per_s": round(g_ach, 1), "probe_G_per_s": best["Ggather_s"],
                                   "frac": round(g_ach / best["Ggather_s"], 3),
@@ -412,6 +413,30 @@ def main():
                                  "sample": f"full c2 SpMV repeated {reps1}x over ~5 s, one OpenMP thread"}
         finally:
             gomp.omp_set_num_threads(len(os.sched_getaffinity(0)))
+
+    # BASELINE configs[3]: PageRank on the it-2004-shaped graph (41.3 M vertices, 1.15 B edges,
+    # x beyond L2) on this GPU; generation (~3 min) and the solver build are outside the timing
+    if rank == 0 and world == 1 and not args.no_extras and not args.no_c4:
+        try:
+            t_g = time.time()
+            G4 = graphgen.make_graph("c4")
+            gen_s = time.time() - t_g
+            t_b = time.time()
+            s4 = pkg.Solver("pagerank", G4.n, G4.row_ptr, G4.col, device=local)
+            build_s = time.time() - t_b
+            s4.run()
+            i4 = s4.run()
+            extras["c4_pagerank_iters_per_s"] = round(1e3 * i4["iterations"] / i4["ms_total"], 1)
+            extras["c4_pagerank_iterations"] = i4["iterations"]
+            extras["c4_pagerank_us_per_iter"] = round(i4["us_per_iter"], 1)
+            extras["c4_pagerank_predicted_us_per_iter"] = round(i4["predicted_us_per_iter"], 1)
+            extras["c4_workload"] = f"it-2004-shaped Graph500 R-MAT s26, n={G4.n}, m={G4.m}, pattern, 1 GPU"
+            extras["c4_gen_s"] = round(gen_s, 1)
+            extras["c4_build_s"] = round(build_s, 1)
+            s4.close()
+            del G4
+        except Exception as ex:
+            extras["c4_error"] = str(ex)[:300]
 
     # row-partitioned PageRank over all ranks (Sec. 3.2): one NCCL allgather per iteration
     if world > 1 and not os.environ.get("TCSPMV_BENCH_NO_DIST"):
