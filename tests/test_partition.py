@@ -393,3 +393,28 @@ def test_gloo_rwr_protocol(tmp_path):
     ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, q, fixed_iters=iters)
     for rk in range(world):
         assert np.abs(np.load(tmp_path / f"r{rk}.npy") - ref).sum() < 1e-12
+
+
+def test_grid_volume_brute_force():
+    """bench/exchange_volume.grid_volume (the 2-D partition of P:L106-L108) against a set
+    computation on a small graph: x values each rank's columns need from other owners plus the
+    partial-y rows it sends to other owners."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("ev", os.path.join(root, "bench", "exchange_volume.py"))
+    ev = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ev)
+    rp, col, _ = graphgen.random_csr(300, 300, 3000, seed=4, kind="powerlaw", valued=False)
+    for P in (2, 4, 6, 8):
+        owner = np.random.default_rng(P).integers(0, P, 300).astype(np.int32)
+        got, shape = ev.grid_volume(rp, col, owner, P)
+        pr, pc = map(int, shape.split("x"))
+        xs, ys = set(), set()
+        for v in range(300):
+            for u in col[rp[v]:rp[v + 1]]:
+                h = (owner[v] // pc) * pc + owner[u] % pc
+                if owner[u] != h:
+                    xs.add((h, int(u)))
+                if owner[v] != h:
+                    ys.add((h, v))
+        assert got == len(xs) + len(ys) and pr * pc == P
