@@ -114,9 +114,56 @@ def dram_regime():
     print(json.dumps(tab["mode3_ratio"]))
 
 
+# Workloads up to the paper's table bound ("WL ... at most 32768"), for Alg. 2's B200
+# candidate set (reading R21): shapes with 4096 < w*h <= 32768, uncached regimes (0, 2) and both
+# value types, one full wave of resident warps each; merged into the existing table, mode 3 (x
+# beyond L2) derived from the stored DRAM/L2 ratios.
+LARGE_RM = [(8192, 1), (16384, 1), (32768, 1), (2048, 4), (4096, 4), (8192, 4), (512, 16), (1024, 16),
+            (2048, 16), (256, 32), (512, 32), (1024, 32)]
+LARGE_CM = [(1, 8192), (1, 16384), (1, 32768), (2, 4096), (2, 8192), (4, 2048), (4, 4096), (8, 1024),
+            (8, 2048), (8, 4096), (16, 512), (16, 1024), (16, 2048), (31, 512), (31, 1024)]
+
+
+def extend():
+    path = os.path.join(ROOT, "paper_1103_2405_b200", "data", "perf_table_b200.json")
+    with open(path) as f:
+        tab = json.load(f)
+    resident = int(tab.get("max_act_warp", 148 * 32))
+    t0 = time.time()
+    new = []
+    for valued in (True, False):
+        for mode in (0, 2):
+            for kind, shapes in (("rm", LARGE_RM), ("cm", LARGE_CM)):
+                for w, h in shapes:
+                    target = int(min(max(8_000_000, resident * w * h), 160_000_000))
+                    sps, ms, _ = measure(kind, w, h, mode, valued, target, reps=3)
+                    new.append([mode, int(valued), KIND[kind], w, h, round(sps, 1)])
+                    print(json.dumps(dict(mode=mode, valued=valued, kind=kind, w=w, h=h, slots_per_s=round(sps),
+                                          ms=round(ms, 3), t=round(time.time() - t0))), flush=True)
+    ratio = {}
+    for k, v in tab.get("mode3_ratio", {}).items():
+        vv, kk = k.split(",")
+        ratio[(int(vv.split("=")[1] == "True") if "True" in vv or "False" in vv else int(vv.split("=")[1]),
+               int(kk.split("=")[1]))] = v
+    have = {(e[0], e[1], e[2], e[3], e[4]) for e in tab["entries"]}
+    for e in new:
+        if (e[0], e[1], e[2], e[3], e[4]) not in have:
+            tab["entries"].append(e)
+        if e[0] == 0 and (e[1], e[2]) in ratio:
+            tab["entries"].append([3, e[1], e[2], e[3], e[4], round(e[5] * ratio[(e[1], e[2])], 1)])
+    tab["max_wl_calibrated"] = 32768
+    for p in (path, os.path.join(ROOT, "gpurun_out", "perf_table_b200.json")):
+        os.makedirs(os.path.dirname(p), exist_ok=True)
+        with open(p, "w") as f:
+            json.dump(tab, f, indent=0)
+    print(json.dumps({"added": len(new), "entries": len(tab["entries"]), "seconds": round(time.time() - t0)}))
+
+
 def main():
     if "--dram" in sys.argv:
         return dram_regime()
+    if "--extend" in sys.argv:
+        return extend()
     quick = "--quick" in sys.argv
     rm_w = [8, 32, 128, 512, 2048] if quick else [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
     rm_h = [1, 4, 16, 32] if quick else [1, 2, 4, 8, 16, 32]

@@ -74,7 +74,8 @@ typedef struct {
     const char* perf_table_path; /* JSON offline table (Sec. 3.3); NULL = built-in B200 table */
     int32_t orient;          /* workload orientation (§8(f) f2 ablations; the model covers the
                                 single-format cases): 0 = composite (Alg. 3: row major iff
-                                w >= h), 1 = row major only (CSR-vector), 2 = column major only (ELL).
+                                w >= h), 1 = row major only (CSR-vector), 2 = column major only (ELL),
+                                -1 = the one the performance model predicts fastest.
                                 Rows of length 0 and split chunks are unaffected. */
     int32_t two_phase;       /* execution of the tiles: -1 = chosen by the performance
                                 model (default), 0 = one-pass tiles (x gathered through L1/L2),
@@ -119,6 +120,8 @@ typedef struct {
     int64_t pb_chunks, pb_bins, pb_long_bins;
     double one_pass_predicted_us;  /* model estimate of the one-pass tiles (Alg. 3 / Eq. 2) */
     double two_phase_predicted_us; /* model estimate of the two-phase tiles */
+    int32_t orient;             /* workload orientation in use (0 composite, 1 row major, 2 column
+                                   major; with spmv_options.orient = -1 the model's choice) */
 } spmv_plan_stats_t;
 
 /* Host view of the layout arrays (Format v1), valid while the plan lives, when the

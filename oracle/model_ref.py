@@ -70,6 +70,26 @@ def partition(row_len, perf, max_act_warp: int, warp: int = 32):
     return opt_wl, opt_time
 
 
+def b200_candidates(longest: int, cap: int = 32768, limit: int = 96):
+    """Reading R21 (B200 mode, rows longer than WL split): the candidate WLs of Alg. 2 are the
+    powers of two from 32 up and the multiples of the longest row, both up to
+    max(longest, cap) (cap: the table bound); at most `limit` multiples."""
+    L = max(1, longest)
+    up = max(L, cap)
+    c = set()
+    v = 32
+    while v <= up:
+        c.add(v)
+        v *= 2
+    k = L
+    n = 0
+    while k <= up and n < limit:
+        c.add(k)
+        k += L
+        n += 1
+    return sorted(c)
+
+
 def tile_count(collen_sorted, n_cols: int, tile_width: int) -> int:
     """Alg. 1 lines 3-8 with reading R10 (continue while NTile*TW < n)."""
     nt = 0

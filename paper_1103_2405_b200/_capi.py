@@ -37,7 +37,7 @@ class PlanStats(ctypes.Structure):
                 ("composite_threshold", c_i32 * 64), ("resident_warps", c_i32),
                 ("perf_table_loaded", c_i32), ("two_phase", c_i32), ("pb_groups", c_i32),
                 ("pb_chunks", c_i64), ("pb_bins", c_i64), ("pb_long_bins", c_i64),
-                ("one_pass_predicted_us", c_f64), ("two_phase_predicted_us", c_f64)]
+                ("one_pass_predicted_us", c_f64), ("two_phase_predicted_us", c_f64), ("orient", c_i32)]
 
 
 class LayoutView(ctypes.Structure):

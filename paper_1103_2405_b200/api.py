@@ -77,7 +77,7 @@ def _stats_dict(s: C.PlanStats) -> dict:
                 two_phase=bool(s.two_phase), pb_groups=s.pb_groups, pb_chunks=s.pb_chunks,
                 pb_bins=s.pb_bins, pb_long_bins=s.pb_long_bins,
                 one_pass_predicted_us=s.one_pass_predicted_us,
-                two_phase_predicted_us=s.two_phase_predicted_us)
+                two_phase_predicted_us=s.two_phase_predicted_us, orient=s.orient)
 
 
 class Plan:

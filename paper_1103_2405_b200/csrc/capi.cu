@@ -223,7 +223,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     auto t0 = std::chrono::steady_clock::now();
     spmv_options opt;
     if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
-    if (opt.orient < 0 || opt.orient > 2) { set_error("orient must be 0, 1 or 2"); return SPMV_EINVAL; }
+    if (opt.orient < -1 || opt.orient > 2) { set_error("orient must be -1, 0, 1 or 2"); return SPMV_EINVAL; }
     if (device >= 0 && (opt.ell_h != 32 || opt.align_rm % 4 != 0)) {
         set_error("device plans need ell_h = 32 and align_rm % 4 == 0"); return SPMV_EINVAL;
     }
@@ -281,7 +281,8 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     }
     {
         Range r("pack_layout");
-        st = pack_layout(P, bp, p->L);
+        p->orient = bp.orient;
+    st = pack_layout(P, bp, p->L);
     }
     if (st) { delete p; return st; }
     p->perm = std::move(P.perm);
@@ -662,6 +663,7 @@ spmv_status spmv_plan_stats(spmv_plan p, spmv_plan_stats_t* o) {
     o->resident_warps = p->grid_tile.empty() ? 0 : p->grid_tile.back() * kWarps;
     o->perf_table_loaded = p->perf_table_loaded;
     o->two_phase = p->two_phase ? 1 : 0;
+    o->orient = p->orient;
     o->pb_groups = p->pb_groups; o->pb_chunks = p->pb_chunks; o->pb_bins = p->pb_bins; o->pb_long_bins = p->pb_long;
     o->one_pass_predicted_us = p->one_pass_us; o->two_phase_predicted_us = p->two_phase_us;
     if (p->two_phase) o->resident_warps = p->pb_grid * kPbWarps;

@@ -22,6 +22,7 @@ struct spmv_plan_s {
     std::vector<tc::TileInfo> tiles;
     double predicted_us = 0.0, build_ms = 0.0;
     int32_t perf_table_loaded = 0;
+    int32_t orient = 0;                 // workload orientation in use (the model's choice for -1)
     // device
     tc::WlDesc* d_desc = nullptr;
     uint32_t* d_row_id = nullptr;

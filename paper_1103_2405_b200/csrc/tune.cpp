@@ -261,7 +261,15 @@ static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist,
     for (auto& h : hist) nnz += h.first * h.second;
     std::vector<int64_t> cand;
     if (bp.split) {
-        for (int64_t c = 256; c <= 1024; c *= 2) cand.push_back(c);   // range the calibration covers
+        // reading R21: rows longer than WL are split, so WL is free: powers of two from one warp's
+        // slots up, and the paper's multiples of the longest row, up to max(WL_low, 32768) (the
+        // paper's table bound)
+        const int64_t up = std::max<int64_t>(L, 32768);
+        for (int64_t c = 32; c <= up; c *= 2) cand.push_back(c);
+        int nm = 0;
+        for (int64_t c = L; c <= up && nm < 96; c += L, ++nm) cand.push_back(c);
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
     } else {
         const int64_t up = std::max<int64_t>(L, nnz / std::max(1, T.max_act_warp));
         for (int64_t c = L; c <= up && cand.size() < 64; c += L) cand.push_back(c);
@@ -322,6 +330,23 @@ static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildPa
 
 spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_count,
                           BuildParams& bp, std::vector<double>& pred_us, int32_t* table_loaded) {
+    if (opt.orient == -1) {
+        // CSR-vector (row major only) and ELL (column major only) are special cases of the
+        // tile-composite model; "the best predicted kernel can be chosen" -- evaluate all three
+        double best = INFINITY;
+        for (int32_t o : {0, 1, 2}) {
+            spmv_options oo = opt;
+            oo.orient = o;
+            BuildParams b;
+            std::vector<double> pr;
+            spmv_status st = choose_params(P, oo, sm_count, b, pr, table_loaded);
+            if (st) return st;
+            double tot = 0.0;
+            for (double u : pr) tot += u;
+            if (tot < best) { best = tot; bp = b; pred_us = pr; }
+        }
+        return SPMV_OK;
+    }
     bp.align_rm = opt.align_rm;
     bp.split = opt.split_long_rows != 0;
     bp.camping = opt.camping_pad != 0;

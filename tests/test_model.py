@@ -71,7 +71,8 @@ def test_predicted_time_equals_transcription(seed, tail, orient, tmp_path):
 
 
 def test_autotuned_wl_is_argmin(tmp_path):
-    """Alg. 2 (B200 candidates 256..1024): the chosen WL minimises the model (strict <, R22)."""
+    """Alg. 2 (B200 candidates, reading R21): the chosen WL minimises the model over the powers of
+    two and the multiples of the longest row up to max(longest, 32768) (strict <, R22)."""
     from paper_1103_2405_b200 import Plan
     table = write_table(tmp_path)
     G = graphgen.make_graph("t_small")
@@ -81,7 +82,7 @@ def test_autotuned_wl_is_argmin(tmp_path):
     st = p.stats()
     hists = tile_hists(G.n, G.n, rp, col, tw, T)
     for t in range(T + 1):
-        cands = [256, 512, 1024]
+        cands = model_ref.b200_candidates(hists[t][0][0] if hists[t] else 1)
         times = [model_ref.pm_packed(hists[t], c, lambda k, w, h: PERF[k], TABLE["max_act_warp"]) for c in cands]
         best = cands[int(np.argmin(times))]       # argmin keeps the first (smallest) on ties
         assert st["wl"][t] == best, (t, st["wl"][t], best, times)
@@ -138,3 +139,19 @@ def test_x_regime_per_tile(stage, budget, tmp_path):
                                     launch_us=TABLE["launch_us"], stage_GBps=TABLE["stage_GBps"],
                                     rmw_GBps=TABLE["rmw_GBps"])
         assert math.isclose(st["tile_predicted_us"][t], us, rel_tol=1e-9), (t, mode, st["tile_predicted_us"][t], us)
+
+
+def test_model_chooses_orientation(tmp_path):
+    """orient = -1: the plan takes the orientation (composite, CSR-vector, ELL) with the
+    smallest predicted time; its prediction equals that orientation's own plan's."""
+    from paper_1103_2405_b200 import Plan
+    table = write_table(tmp_path)
+    rp, col, _ = graphgen.random_csr(3000, 3000, 60000, seed=7, kind="powerlaw", valued=False)
+    pred = {}
+    for o in (0, 1, 2):
+        st = Plan(3000, 3000, rp, col, None, device=-1, orient=o, perf_table_path=table, two_phase=0).stats()
+        pred[o] = st["predicted_us"]
+        assert st["orient"] == o
+    st = Plan(3000, 3000, rp, col, None, device=-1, orient=-1, perf_table_path=table, two_phase=0).stats()
+    best = min(pred, key=lambda o: (pred[o], o))
+    assert st["orient"] == best and math.isclose(st["predicted_us"], pred[best], rel_tol=1e-12), (pred, st["orient"])

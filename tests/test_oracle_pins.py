@@ -537,3 +537,14 @@ def test_tile_time_us_terms_by_hand():
     assert math.isclose(us0, waves + 3.0, rel_tol=1e-12)
     assert model_ref.tile_time_us([], 100, lambda k, w, hh: 1e9, 4, tile_index=1, tile_width=8, cached=True,
                                   launch_us=3.0, stage_GBps=1.0, rmw_GBps=1.0) == 0.0
+
+
+def test_b200_candidate_set_by_hand():
+    """Reading R21: powers of two from 32 to max(L, 32768) plus the first 96 multiples of the
+    longest row L that do not exceed it (table bound)."""
+    c = model_ref.b200_candidates(100)
+    assert [v for v in c if v & (v - 1) == 0] == [32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768]
+    assert [v for v in c if v % 100 == 0] == [100 * k for k in range(1, 97)]
+    assert len(c) == 11 + 96              # no power of two is a multiple of 100 (25 does not divide it)
+    c = model_ref.b200_candidates(50000)
+    assert c[-1] == 50000 and 32768 in c and 65536 not in c and len(c) == 12
