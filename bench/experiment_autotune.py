@@ -3,7 +3,9 @@ Chung-Lu graphs over the power-law exponent sweep, compare the auto-tuned plan (
 measured offline table) against an exhaustive search over tile count and workload size, and the
 model's predicted time against the measured time.
 
-Usage (GPU box): python bench/experiment_autotune.py [--quick] > profiles/r01_autotune.json
+The one-pass tiles are tuned (two_phase = 0: Alg. 1-3 is the paper's tuner); the two-phase time
+is reported beside it.  --c2 adds the LiveJournal-shaped graph.
+Usage (GPU box): python bench/experiment_autotune.py [--quick] [--c2] > profiles/r02_autotune.json
 """
 import ctypes
 import json
@@ -41,28 +43,38 @@ def main():
         shapes = {g: shapes[g]}
     tile_counts = (0,) if "--t0" in sys.argv else (0, 1, 2, 4)
     out = []
-    for name, (n, m) in shapes.items():
-        for a in alphas:
-            keys = graphgen.chung_lu_edges(n, m, a, 2e4)
-            G = graphgen.graph_from_keys(f"{name}_a{a}", n, keys)
+    cases = [(name, n, m, a) for name, (n, m) in shapes.items() for a in alphas]
+    if "--c2" in sys.argv:
+        cases.insert(0, ("c2", None, None, None))
+    for name, n, m, a in cases:
+        if True:
+            if name == "c2":
+                G = graphgen.make_graph("c2")
+                n = G.n
+            else:
+                keys = graphgen.chung_lu_edges(n, m, a, 2e4)
+                G = graphgen.graph_from_keys(f"{name}_a{a}", n, keys)
             val = graphgen.edge_values(G.keys)
             x = graphgen.uniform_f32(n, seed=graphgen.SEED_X)
             xt = torch.from_numpy(x).cuda()
             yt = torch.empty(n, device="cuda")
-            auto = pkg.Plan(n, n, G.row_ptr, G.col, val, device=0)
+            auto = pkg.Plan(n, n, G.row_ptr, G.col, val, device=0, two_phase=0)
             st = auto.stats()
             auto_us = time_plan(auto, xt, yt)
             auto_launch = st["predicted_us"]
             auto.close()
+            tp = pkg.Plan(n, n, G.row_ptr, G.col, val, device=0, two_phase=1)
+            tp_us, tp_pred = time_plan(tp, xt, yt), tp.stats()["two_phase_predicted_us"]
+            tp.close()
             best = None
             grid = []
             for tw in (24576, 49152):
                 for T in tile_counts:
                     if T == 0 and tw != 24576:
                         continue
-                    for wl in (256, 512, 1024):
+                    for wl in (256, 512, 1024, 2048, 4096, 8192):
                         p = pkg.Plan(n, n, G.row_ptr, G.col, val, device=0, tile_width=tw, num_tiles=T,
-                                     workload_size=wl)
+                                     workload_size=wl, two_phase=0)
                         s2 = p.stats()
                         us = time_plan(p, xt, yt)
                         grid.append(dict(tile_width=tw, num_tiles=s2["num_tiles"], wl=wl, us=round(us, 2),
@@ -77,10 +89,11 @@ def main():
                        exhaustive_best=best,
                        auto_vs_best=round(best["us"] / auto_us, 4),
                        prediction_error=round(abs(auto_launch - auto_us) / auto_us, 4),
+                       two_phase=dict(us=round(tp_us, 2), predicted_us=round(tp_pred, 2)),
                        grid=grid)
             out.append(rec)
             print(json.dumps({k: rec[k] for k in ("graph", "alpha", "auto", "exhaustive_best", "auto_vs_best",
-                                                  "prediction_error")}), file=sys.stderr, flush=True)
+                                                  "prediction_error", "two_phase")}), file=sys.stderr, flush=True)
     print(json.dumps(out))
 
 

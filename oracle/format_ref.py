@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-KIND_RM, KIND_CM, KIND_SPLIT = 0, 1, 2
+KIND_RM, KIND_CM, KIND_SPLIT, KIND_COO = 0, 1, 2, 3
+COO_END = 1 << 31          # TILE-COO: flags the last entry of each row in its column word
 FLAG_ACC = 1 << 29       # row already written by an earlier tile: add instead of store
 FLAG_FINAL = 1 << 30     # no later tile touches this row: its value is final after this write
 PAD_ROW = 0xFFFFFFFF     # padding row of a column-major slab (no write)
@@ -149,10 +150,36 @@ def build(n_rows, n_cols, row_ptr, col, val, tile_width, num_tiles, workload_siz
         tiles[t, 0], tiles[t, 1] = lo, hi
         tiles[t, 2] = len(desc["off"])
         i = 0
+        coo = orient == 3 and t < T               # TILE-COO: COO dense tiles
+        orient_t = 0 if orient == 3 else orient   # ... and a composite remainder (R19)
         while i < len(rows):
             w = lens[i]
             hq = max(1, WL // max(w, 1))          # Alg. 3 line 9 (R12)
             cur_off = len(slot_col)
+            if coo and not (split_long_rows and w > WL):
+                # whole rows while the workload holds at most WL entries (at least one row), back
+                # to back, the last entry of each row flagged (bit 31 of the column), padded to 32
+                h, tot = 0, 0
+                while i + h < len(rows) and (h == 0 or tot + lens[i + h] <= WL):
+                    tot += lens[i + h]
+                    h += 1
+                wp = _roundup(tot, 32)
+                emit(cur_off, len(row_id), wp, h, KIND_COO, 1, -1, 0)
+                for r in rows[i:i + h]:
+                    row_id.append(flags_for(t, r))
+                    ents = per_tile[t][r]
+                    for k, (c_, v_) in enumerate(ents):
+                        word = c_ | (COO_END if k + 1 == len(ents) else 0)
+                        slot_col.append(word - (1 << 32) if word >= (1 << 31) else word)   # as int32
+                        if not pattern:
+                            slot_val.append(v_)
+                for _ in range(wp - tot):
+                    slot_col.append(sentinel)
+                    if not pattern:
+                        slot_val.append(np.float32(0))
+                camp()
+                i += h
+                continue
             if split_long_rows and w > WL:        # R21: one-row chunks of <= WL entries
                 r = rows[i]
                 ents = per_tile[t][r]
@@ -180,7 +207,7 @@ def build(n_rows, n_cols, row_ptr, col, val, tile_width, num_tiles, workload_siz
                 continue
             # Alg. 3's rule (row major iff w >= h); orient 1 / 2 force one format for the
             # single-format special cases the model covers, zero-length rows excepted
-            if (w > 0) if orient == 1 else (False if orient == 2 else w >= hq):   # row major
+            if (w > 0) if orient_t == 1 else (False if orient_t == 2 else w >= hq):   # row major
                 h = min(hq, len(rows) - i)
                 wp = _roundup(w, align_rm)
                 emit(cur_off, len(row_id), wp, h, KIND_RM, 4, -1, 0)
@@ -262,13 +289,21 @@ def decode_to_coo(L: Layout):
         kind, kvec = int(L.desc["kind"][j]), int(L.desc["kvec"][j])
 
         def put(r_entry, s):
-            c = int(L.slot_col[s])
+            c = int(L.slot_col[s]) & (COO_END - 1)
             if c == sent:
                 return
             rows.append(int(r_entry) & (FLAG_ACC - 1))
             cols.append(int(L.perm[lo + c]))
             vals.append(1.0 if L.pattern else float(L.slot_val[s]))
-        if kind in (KIND_RM, KIND_SPLIT):
+        if kind == KIND_COO:
+            r = 0
+            for k in range(w):
+                if r >= h:
+                    break
+                put(L.row_id[rb + r], off + k)
+                if int(L.slot_col[off + k]) < 0:          # bit 31: the row's last entry
+                    r += 1
+        elif kind in (KIND_RM, KIND_SPLIT):
             for r in range(h):
                 for k in range(w):
                     put(L.row_id[rb + r], off + r * w + k)

@@ -117,6 +117,17 @@ def packed_workloads(hist, WL, align=8, split=True, ell_h=32, orient=0):
     while i < len(rows):
         w = rows[i]
         hq = max(1, WL // max(w, 1))
+        if orient == 3 and not (split and w > WL):
+            # TILE-COO (dense tiles): whole rows while at most WL entries (at least one),
+            # padded to 32 slots; charged at the row-major table shape (slots, 1)
+            h, tot = 0, 0
+            while i + h < len(rows) and (h == 0 or tot + rows[i + h] <= WL):
+                tot += rows[i + h]
+                h += 1
+            wp = _rup(tot, 32)
+            out.append(("rm", wp, 1, wp))
+            i += h
+            continue
         if split and w > WL:
             c = 0
             while c * WL < w:
@@ -124,7 +135,7 @@ def packed_workloads(hist, WL, align=8, split=True, ell_h=32, orient=0):
                 out.append(("rm", wp, 1, wp))
                 c += 1
             i += 1
-        elif ((w > 0) if orient == 1 else (False if orient == 2 else w >= hq)):
+        elif ((w > 0) if orient == 1 else (False if orient == 2 else w >= hq)):   # orient 3: composite here
             h = min(hq, len(rows) - i)
             wp = _rup(w, align)
             out.append(("rm", wp, h, h * wp))

@@ -246,9 +246,25 @@ spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L)
         auto camp = [&](int64_t size) {
             if (bp.camping && size > 0 && size % 512 == 0) n_slots += 64;
         };
+        // TILE-COO: the dense tiles as COO workloads, the remainder composite (R19)
+        const bool coo = bp.orient == 3 && t < T;
+        const int32_t orient_t = bp.orient == 3 ? 0 : bp.orient;
         while (i < nr) {
             int64_t w = len_of(rows[i]);
             int64_t hq = std::max<int64_t>(1, WL / std::max<int64_t>(w, 1));
+            if (coo && !(bp.split && w > WL)) {
+                // whole rows while the workload holds at most WL entries (at least one row), padded
+                // to a multiple of 32 slots: a row never crosses a workload (one writer per row)
+                int64_t h = 0, tot = 0;
+                while (i + h < nr && (h == 0 || tot + len_of(rows[i + h]) <= WL)) tot += len_of(rows[i + h++]);
+                const int64_t wp = roundup(tot, 32);
+                L.desc.push_back(WlDesc{n_slots, (int32_t)L.row_id.size(), (int32_t)wp, (int32_t)h, KIND_COO, 1, 0, -1, 0});
+                for (int64_t r = 0; r < h; ++r) L.row_id.push_back(entry_of(rows[i + r]));
+                n_slots += wp;
+                camp(wp);
+                i += h;
+                continue;
+            }
             if (bp.split && w > WL) {
                 int32_t r = rows[i];
                 int64_t nch = (w + WL - 1) / WL;
@@ -268,7 +284,7 @@ spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L)
                 ++i;
                 continue;
             }
-            if (row_major(bp.orient, w, hq)) {
+            if (row_major(orient_t, w, hq)) {
                 int64_t h = std::min<int64_t>(hq, nr - i);
                 int64_t wp = roundup(w, align);
                 L.desc.push_back(WlDesc{n_slots, (int32_t)L.row_id.size(), (int32_t)wp, (int32_t)h, KIND_RM, 4, 0, -1, 0});
@@ -318,6 +334,17 @@ spmv_status pack_layout(const Prepared& P, const BuildParams& bp, HostLayout& L)
                 for (int64_t k = 0; k < part; ++k) {
                     L.slot_col[d.off + k] = (int32_t)(P.kcol[src + k] - lo);
                     if (!P.pattern) L.slot_val[d.off + k] = P.kval[src + k];
+                }
+            } else if (d.kind == KIND_COO) {
+                int64_t dst = d.off;
+                for (int32_t rr = 0; rr < d.h; ++rr) {
+                    int32_t r = (int32_t)(L.row_id[d.row_base + rr] & ROW_MASK);
+                    int64_t src = seg_start[r], cnt = seg_len[r];
+                    for (int64_t k = 0; k < cnt; ++k) {
+                        L.slot_col[dst + k] = (int32_t)((uint32_t)(P.kcol[src + k] - lo) | (k + 1 == cnt ? COO_END : 0u));
+                        if (!P.pattern) L.slot_val[dst + k] = P.kval[src + k];
+                    }
+                    dst += cnt;
                 }
             } else if (d.kind == KIND_RM) {
                 for (int32_t rr = 0; rr < d.h; ++rr) {

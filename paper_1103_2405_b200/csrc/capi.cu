@@ -223,7 +223,7 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     auto t0 = std::chrono::steady_clock::now();
     spmv_options opt;
     if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
-    if (opt.orient < -1 || opt.orient > 2) { set_error("orient must be -1, 0, 1 or 2"); return SPMV_EINVAL; }
+    if (opt.orient < -1 || opt.orient > 3) { set_error("orient must be -1, 0, 1, 2 or 3"); return SPMV_EINVAL; }
     if (device >= 0 && (opt.ell_h != 32 || opt.align_rm % 4 != 0)) {
         set_error("device plans need ell_h = 32 and align_rm % 4 == 0"); return SPMV_EINVAL;
     }
@@ -829,7 +829,7 @@ spmv_status spmv_plan_to_coo(spmv_plan p, int32_t* rows, int32_t* cols, float* v
         for (int64_t j = ti.wl_begin; j < ti.wl_end; ++j) {
             const WlDesc& d = L.desc[j];
             auto put = [&](uint32_t ent, int64_t slot) {
-                int32_t c = L.slot_col[slot];
+                int32_t c = (int32_t)((uint32_t)L.slot_col[slot] & ~COO_END);
                 if (c == sent) return;
                 if (w >= p->nnz) return;
                 rows[w] = (int32_t)(ent & ROW_MASK);
@@ -837,7 +837,14 @@ spmv_status spmv_plan_to_coo(spmv_plan p, int32_t* rows, int32_t* cols, float* v
                 if (vals) vals[w] = p->pattern ? 1.0f : L.slot_val[slot];
                 ++w;
             };
-            if (d.kind != KIND_CM) {
+            if (d.kind == KIND_COO) {           // rows back to back, COO_END closes each
+                int32_t r = 0;
+                for (int32_t k = 0; k < d.w && r < d.h; ++k) {
+                    const int64_t slot = d.off + k;
+                    put(L.row_id[d.row_base + r], slot);
+                    if ((uint32_t)L.slot_col[slot] & COO_END) ++r;
+                }
+            } else if (d.kind != KIND_CM) {
                 for (int32_t r = 0; r < d.h; ++r)
                     for (int32_t k = 0; k < d.w; ++k) put(L.row_id[d.row_base + r], d.off + (int64_t)r * d.w + k);
             } else {

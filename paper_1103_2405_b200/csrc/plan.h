@@ -12,7 +12,10 @@ constexpr uint32_t FLAG_ACC = 1u << 29;    // row already written by an earlier 
 constexpr uint32_t FLAG_FINAL = 1u << 30;  // no later tile touches the row: value is final
 constexpr uint32_t ROW_MASK = (1u << 29) - 1;
 constexpr uint32_t PAD_ROW = 0xFFFFFFFFu;  // padding row of a column-major slab
-enum : uint8_t { KIND_RM = 0, KIND_CM = 1, KIND_SPLIT = 2 };
+enum : uint8_t { KIND_RM = 0, KIND_CM = 1, KIND_SPLIT = 2, KIND_COO = 3 };
+// TILE-COO workloads (orient = 3, dense tiles): whole rows back to back, the last slot of
+// each row carries this flag in its column word
+constexpr uint32_t COO_END = 1u << 31;
 
 // One warp's workload (Solution 3): a w x h rectangle of slots.  32 bytes, read once per warp.
 struct WlDesc {
@@ -73,7 +76,8 @@ struct BuildParams {
     bool split = true;
     bool camping = false;
     int32_t ell_h = 32;
-    int32_t orient = 0;               // 0 composite, 1 row major only, 2 column major only
+    int32_t orient = 0;               // 0 composite, 1 row major only, 2 column major only,
+                                      // 3 TILE-COO (dense tiles COO, remainder composite)
 };
 
 // Alg. 3's orientation rule (row major iff w >= h), or a forced single format (f2 ablations).

@@ -315,6 +315,48 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
     }
 }
 
+// TILE-COO workload (Observation 3): whole rows back to back, the last slot of each row
+// flagged (COO_END).  The warp takes 32 slots per step, one per lane, and sums each row with a
+// segmented inclusive scan over the lanes (Hillis-Steele with head flags: the paper's "binary
+// reduction" that checks whether two operands belong to the same row, done with shuffles instead
+// of serialised branches); the row open at the end of a step carries into the next.  Lanes that
+// end a row write it (row index = rows ended before it in the workload).  Fixed order:
+// deterministic.
+template <bool VALUED, bool SMEM, class X, class Epi>
+__device__ __forceinline__ void run_coo(const TileArgs& a, const WlDesc& d, const int32_t* wc,
+                                        const float* wv, const X& x, Epi& epi, int lane) {
+    float carry = 0.0f;                      // sum of the row open at the start of the step
+    int32_t row = 0;                         // rows ended before this step
+    for (int s0 = 0; s0 < d.w; s0 += 32) {
+        const uint32_t cw = (uint32_t)(SMEM ? wc[s0 + lane] : __ldcs(wc + s0 + lane));
+        const bool end = (cw & COO_END) != 0u;
+        const int32_t c = (int32_t)(cw & ~COO_END);
+        float v = x(c);                       // sentinel (padding) -> 0
+        if (VALUED) v *= SMEM ? wv[s0 + lane] : __ldcs(wv + s0 + lane);
+        const unsigned ends = __ballot_sync(0xffffffffu, end);
+        // head of a segment: lane 0 or the lane after a row end
+        bool head = lane == 0 || ((ends >> (lane - 1)) & 1u);
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float t = __shfl_up_sync(0xffffffffu, v, o);
+            const bool th = __shfl_up_sync(0xffffffffu, head, o);
+            if (lane >= o && !head) { v += t; head = th; }
+        }
+        // lanes of the step's first segment continue the row carried in
+        const unsigned first_end = ends ? (unsigned)__ffs(ends) - 1u : 32u;
+        if ((unsigned)lane <= first_end) v += carry;
+        if (end) {
+            const int32_t r = row + __popc(ends & ((1u << lane) - 1u));
+            const uint32_t ent = __ldg(a.row_id + d.row_base + r);
+            epi.write(ent, d.row_base + r, v);
+        }
+        // the open row's running sum (lane 31 when it does not end a row)
+        const float last = __shfl_sync(0xffffffffu, v, 31);
+        carry = (ends >> 31) & 1u ? 0.0f : last;
+        row += __popc(ends);
+    }
+}
+
 // zero-length rows (remainder tile): every row of every slab gets value 0
 template <class Epi>
 __device__ __forceinline__ void run_zero(const TileArgs& a, const WlDesc& d, Epi& epi, int lane) {
@@ -353,7 +395,8 @@ __device__ __forceinline__ WlDesc load_desc(const WlDesc* p) {
 template <bool VALUED, bool SMEM, class X, class Epi>
 __device__ __forceinline__ void run_workload(const TileArgs& a, const WlDesc& d, const int32_t* wc,
                                              const float* wv, const X& x, Epi& epi, int lane) {
-    if (d.kind != KIND_CM) run_rm<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+    if (d.kind == KIND_COO) run_coo<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
+    else if (d.kind != KIND_CM) run_rm<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
     else if (d.w == 0) run_zero(a, d, epi, lane);
     else dispatch_cm<VALUED, SMEM>(a, d, wc, wv, x, epi, lane);
 }

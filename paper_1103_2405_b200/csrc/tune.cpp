@@ -227,13 +227,33 @@ static double pm_tile(const std::vector<std::pair<int64_t, int64_t>>& hist, int6
     while (remaining > 0) {                                  // Alg. 3 lines 7-16 (packing walk)
         const int64_t w = hist[g].first;
         const int64_t hq = std::max<int64_t>(1, WL / std::max<int64_t>(w, 1));
+        if (orient == 3 && !(split && w > WL)) {
+            // TILE-COO workload: whole rows while at most WL entries (at least one), padded to 32
+            // slots; charged at the row-major table shape (w = slots, h = 1)
+            int64_t tot = 0, h = 0, oo = off;
+            size_t gg = g;
+            while (gg < hist.size()) {
+                const int64_t L = hist[gg].first, avail = hist[gg].second - oo;
+                int64_t k = L > 0 ? std::min<int64_t>(avail, (WL - tot) / L) : avail;
+                if (h == 0 && k == 0) k = 1;
+                if (k <= 0) break;
+                tot += k * L; h += k; oo += k;
+                if (oo < hist[gg].second) break;
+                ++gg; oo = 0;
+                if (gg < hist.size() && split && hist[gg].first > WL) break;
+            }
+            const int64_t wp = rup(tot, 32);
+            add(KIND_RM, wp, 1, wp);
+            advance(h);
+            continue;
+        }
         if (split && w > WL) {                               // R21: one-row chunks
             for (int64_t c = 0; c * WL < w; ++c) {
                 const int64_t part = std::min<int64_t>(WL, w - c * WL), wp = rup(part, align);
                 add(KIND_RM, wp, 1, wp);
             }
             advance(1);
-        } else if (row_major(orient, w, hq)) {               // row major
+        } else if (row_major(orient == 3 ? 0 : orient, w, hq)) {   // row major
             const int64_t h = std::min<int64_t>(hq, remaining), wp = rup(w, align);
             add(KIND_RM, wp, h, h * wp);
             advance(h);
@@ -275,11 +295,15 @@ static void partition_tile(const std::vector<std::pair<int64_t, int64_t>>& hist,
         for (int64_t c = L; c <= up && cand.size() < 64; c += L) cand.push_back(c);
         if (cand.empty()) cand.push_back(L);
     }
+    // the candidates are independent model walks: evaluated in parallel, reduced in candidate
+    // order (strict <, so the smallest WL wins ties, R22)
+    std::vector<double> tt(cand.size());
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < (int64_t)cand.size(); ++i)
+        tt[i] = pm_tile(hist, cand[i], bp.align_rm, bp.split, bp.ell_h, cached, valued, T, nullptr, bp.orient);
     opt_t = INFINITY; opt_wl = (int32_t)cand[0];
-    for (int64_t c : cand) {
-        double t = pm_tile(hist, c, bp.align_rm, bp.split, bp.ell_h, cached, valued, T, nullptr, bp.orient);
-        if (t < opt_t) { opt_t = t; opt_wl = (int32_t)c; }
-    }
+    for (size_t i = 0; i < cand.size(); ++i)
+        if (tt[i] < opt_t) { opt_t = tt[i]; opt_wl = (int32_t)cand[i]; }
 }
 
 struct Choice { int32_t tw, T; std::vector<int32_t> wl; std::vector<double> us; double total; };
@@ -307,11 +331,12 @@ static Choice evaluate(const Prepared& P, const spmv_options& opt, const BuildPa
         double sec = 0.0;
         if (opt.workload_sizes) wl = opt.workload_sizes[std::min(t, opt.num_tiles >= 0 ? opt.num_tiles : t)];
         else if (opt.workload_size > 0) wl = opt.workload_size;
+        BuildParams bt = base;                  // TILE-COO: COO dense tiles, composite remainder
+        if (bt.orient == 3 && t == T) bt.orient = 0;
         if (opt.workload_sizes || opt.workload_size > 0) {
-            BuildParams b = base; b.wl.assign(1, wl);
-            sec = pm_tile(hist[t], wl, b.align_rm, b.split, b.ell_h, mode, valued, tab, nullptr, b.orient);
+            sec = pm_tile(hist[t], wl, bt.align_rm, bt.split, bt.ell_h, mode, valued, tab, nullptr, bt.orient);
         } else {
-            partition_tile(hist[t], base, mode, valued, tab, wl, sec);
+            partition_tile(hist[t], bt, mode, valued, tab, wl, sec);
         }
         int64_t rows = 0, nnz = 0;
         for (auto& h : hist[t]) { rows += h.second; nnz += h.first * h.second; }
@@ -332,9 +357,10 @@ spmv_status choose_params(const Prepared& P, const spmv_options& opt, int sm_cou
                           BuildParams& bp, std::vector<double>& pred_us, int32_t* table_loaded) {
     if (opt.orient == -1) {
         // CSR-vector (row major only) and ELL (column major only) are special cases of the
-        // tile-composite model; "the best predicted kernel can be chosen" -- evaluate all three
+        // tile-composite model; "the best predicted kernel can be chosen" -- evaluate them, the
+        // composite and TILE-COO
         double best = INFINITY;
-        for (int32_t o : {0, 1, 2}) {
+        for (int32_t o : {0, 1, 2, 3}) {
             spmv_options oo = opt;
             oo.orient = o;
             BuildParams b;

@@ -292,3 +292,31 @@ def test_plan_import_rejects_garbage(tmp_path):
     f.write_bytes(b"not a plan at all")
     with pytest.raises(SpmvError):
         Plan.load(f, device=-1)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tile_coo_bit_exact(seed):
+    """f2 TILE-COO (orient = 3): the dense tiles as COO workloads (whole rows back to back,
+    row ends flagged), the remainder composite; byte-identical to the oracle builder and decoding
+    to the input (split and paper mode both)."""
+    rng = np.random.default_rng(3000 + seed)
+    nr, nc = int(rng.integers(50, 700)), int(rng.integers(50, 700))
+    valued = seed % 2 == 0
+    rp, col, val = graphgen.random_csr(nr, nc, int(rng.integers(500, 9000)), seed=seed, kind="powerlaw",
+                                       valued=valued)
+    tw = int(rng.integers(4, 80))
+    T = int(rng.integers(1, min((nc + tw - 1) // tw, 5) + 1))
+    wls = [int(rng.integers(8, 400)) for _ in range(T + 1)]
+    split = seed != 3
+    if not split:
+        longest = int(np.diff(rp).max())
+        wls = [max(w, longest) for w in wls]
+    ref, p = build_both(nr, nc, rp, col, val, tw, T, wls, split=split, orient=3)
+    assert_same(ref, p)
+    assert 3 in set(ref.desc["kind"].tolist())
+    r, c, v = format_ref.decode_to_coo(ref)
+    exp_v = np.ones(len(col)) if val is None else val
+    assert sorted(zip(r.tolist(), c.tolist(), v.tolist())) == sorted(
+        zip(np.repeat(np.arange(nr), np.diff(rp)).tolist(), col.tolist(), exp_v.astype(np.float64).tolist()))
+    r2, c2, v2 = p.to_coo()
+    assert sorted(zip(r2.tolist(), c2.tolist())) == sorted(zip(r.tolist(), c.tolist()))

@@ -29,7 +29,8 @@ OPTS = [dict(), dict(tile_width=512, num_tiles=3, workload_size=256),
         dict(num_tiles=0, workload_size=64, stage_x=0),
         # two-phase tiles with small caps: several groups, chunks, bins, long rows
         dict(two_phase=1, pb_region=256, pb_chunk=300, pb_xcap=700, pb_group=20000),
-        dict(two_phase=0)]
+        dict(two_phase=0),
+        dict(orient=3, tile_width=512, num_tiles=3, workload_size=256)]   # TILE-COO dense tiles
 
 
 @pytest.mark.parametrize("opt", range(len(OPTS)))

@@ -46,6 +46,14 @@ CASES = [
     (3000, 3000, 90000, "powerlaw", False, False, dict(orient=1, tile_width=256, num_tiles=2, workload_size=256)),
     (3000, 3000, 90000, "powerlaw", True, True, dict(orient=2)),
     (3000, 3000, 90000, "powerlaw", False, False, dict(orient=2, tile_width=256, num_tiles=2, workload_size=512)),
+    # f2 TILE-COO: COO dense tiles (segmented warp sums), composite remainder
+    (3000, 3000, 90000, "powerlaw", True, True, dict(orient=3, tile_width=256, num_tiles=3, workload_size=256)),
+    (3000, 3000, 90000, "powerlaw", False, False, dict(orient=3, tile_width=64, num_tiles=4, workload_size=40)),
+    (2000, 2000, 50000, "powerlaw", True, False, dict(orient=3, tile_width=512, num_tiles=2, workload_size=96, stage_x=0)),
+    (1000, 5000, 40000, "uniform", True, True, dict(orient=3, tile_width=1000, num_tiles=4, workload_size=5000,
+                                                    split_long_rows=0)),
+    # the model's choice among the four
+    (3000, 3000, 90000, "powerlaw", True, False, dict(orient=-1)),
 ]
 
 

@@ -51,7 +51,7 @@ def expected_us(h, WL, t, T, tw, cached, split=True, tail_frac=0.0, orient=0):
 
 
 @pytest.mark.parametrize("seed,tail,orient", [(0, 0.0, 0), (1, 0.0, 0), (2, 0.0, 0), (3, 0.0, 0), (4, 0.5, 0),
-                                              (5, 0.5, 0), (6, 0.0, 1), (7, 0.5, 2)])
+                                              (5, 0.5, 0), (6, 0.0, 1), (7, 0.5, 2), (8, 0.0, 3), (9, 0.5, 3)])
 def test_predicted_time_equals_transcription(seed, tail, orient, tmp_path):
     from paper_1103_2405_b200 import Plan
     table = write_table(tmp_path, tail_frac=tail)
@@ -66,7 +66,8 @@ def test_predicted_time_equals_transcription(seed, tail, orient, tmp_path):
     assert st["perf_table_loaded"]
     hists = tile_hists(nr, nc, rp, col, tw, T)
     for t in range(T + 1):
-        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T, tail_frac=tail, orient=orient)
+        o_t = 0 if (orient == 3 and t == T) else orient      # TILE-COO: composite remainder
+        exp = expected_us(hists[t], wls[t], t, T, tw, cached=t < T, tail_frac=tail, orient=o_t)
         assert math.isclose(st["tile_predicted_us"][t], exp, rel_tol=1e-9), (t, st["tile_predicted_us"][t], exp)
 
 
@@ -142,13 +143,13 @@ def test_x_regime_per_tile(stage, budget, tmp_path):
 
 
 def test_model_chooses_orientation(tmp_path):
-    """orient = -1: the plan takes the orientation (composite, CSR-vector, ELL) with the
-    smallest predicted time; its prediction equals that orientation's own plan's."""
+    """orient = -1: the plan takes the orientation (composite, CSR-vector, ELL, TILE-COO)
+    with the smallest predicted time; its prediction equals that orientation's own plan's."""
     from paper_1103_2405_b200 import Plan
     table = write_table(tmp_path)
     rp, col, _ = graphgen.random_csr(3000, 3000, 60000, seed=7, kind="powerlaw", valued=False)
     pred = {}
-    for o in (0, 1, 2):
+    for o in (0, 1, 2, 3):
         st = Plan(3000, 3000, rp, col, None, device=-1, orient=o, perf_table_path=table, two_phase=0).stats()
         pred[o] = st["predicted_us"]
         assert st["orient"] == o

@@ -548,3 +548,15 @@ def test_b200_candidate_set_by_hand():
     assert len(c) == 11 + 96              # no power of two is a multiple of 100 (25 does not divide it)
     c = model_ref.b200_candidates(50000)
     assert c[-1] == 50000 and 32768 in c and 65536 not in c and len(c) == 12
+
+
+def test_tile_coo_packing_by_hand():
+    """TILE-COO workloads (orient 3): rows [70, 9, 9, 3, 2, 2, 1], WL 32, split: the row of 70
+    becomes chunks 32, 32, 6 (padded to 8) as in the composite; then whole rows while at most 32
+    entries: 9 + 9 + 3 + 2 + 2 + 1 = 26 -> one workload of 26 entries padded to 32 slots.  With
+    WL 16: {9} (9 + 9 > 16), {9, 3, 2, 2} = 16, {1} -> 16, 16, 32 slots."""
+    h = _hist([70, 9, 9, 3, 2, 2, 1])
+    assert model_ref.packed_workloads(h, 32, align=8, split=True, orient=3) == [
+        ("rm", 32, 1, 32), ("rm", 32, 1, 32), ("rm", 8, 1, 8), ("rm", 32, 1, 32)]
+    assert model_ref.packed_workloads(_hist([9, 9, 3, 2, 2, 1]), 16, orient=3) == [
+        ("rm", 32, 1, 32), ("rm", 32, 1, 32), ("rm", 32, 1, 32)]
