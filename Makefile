@@ -19,7 +19,7 @@ HDRS      := $(wildcard include/*.h) $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/
 CU_OBJS   := $(patsubst $(CSRC)/%.cu,build/%.cu.o,$(CU_SRCS))
 CPP_OBJS  := $(patsubst $(CSRC)/%.cpp,build/%.cpp.o,$(CPP_SRCS))
 
-ALL_TARGETS := graphgen/libgraphgen.so oracle/liboracle.so
+ALL_TARGETS := graphgen/libgraphgen.so oracle/liboracle.so graphgen/libgraphgen_gpu.so
 ifneq ($(strip $(CU_SRCS)),)
 ALL_TARGETS += $(LIBDIR)/libtcspmv.so
 endif
@@ -28,6 +28,10 @@ all: $(ALL_TARGETS)
 
 graphgen/libgraphgen.so: graphgen/graphgen.c
 	$(CC) -O3 -fPIC -shared -fopenmp -fvisibility=hidden -o $@ $<
+
+# the same generator on the device (c4 / c5 sizes, per-rank rows); input infrastructure, not the product
+graphgen/libgraphgen_gpu.so: graphgen/graphgen_gpu.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -o $@ $< -lcudart_static -ldl -lpthread -lrt
 
 oracle/liboracle.so: oracle/oracle.c
 	$(CC) -O2 -fPIC -shared -fopenmp -fvisibility=hidden -o $@ $< -lm

@@ -146,6 +146,11 @@ CONFIGS = {
     "c3_youtube": dict(kind="chung_lu", n=1_100_000, m=4_900_000, alpha=2.2, max_deg=2e4),
     # c4: it-2004 shaped web graph, Graph500 R-MAT scale 26, ids >= n rejected
     "c4": dict(kind="rmat", scale=26, n=41_291_594, m=1_150_725_436, a=0.57, b=0.19, c=0.19),
+    # c5: uk-union shaped web graph, Graph500 R-MAT scale 28, ids >= n rejected (HITS
+    # block 267,266,080 rows, 11,015,359,644 entries).  Device generator only (DeviceGraph): the host
+    # generator would need ~200 GB.  c5_s22: the same shape at 1/64 (dry runs of the c5 route).
+    "c5": dict(kind="rmat", scale=28, n=133_633_040, m=5_507_679_822, a=0.57, b=0.19, c=0.19),
+    "c5_s22": dict(kind="rmat", scale=22, n=2_088_016, m=86_057_497, a=0.57, b=0.19, c=0.19),
     # small parity cases (several tiles + ragged tails, oracle finishes in seconds)
     "t_small": dict(kind="rmat", scale=12, n=4000, m=40_000, a=0.57, b=0.19, c=0.19),
     "t_mid": dict(kind="rmat", scale=17, n=100_000, m=1_200_000, a=0.50, b=0.20, c=0.20),
@@ -220,3 +225,124 @@ def random_csr(n_rows: int, n_cols: int, nnz: int, seed: int = 7, kind: str = "u
     if valued:
         val = (rng.uniform(-1, 1, nnz) if signed else rng.uniform(0, 1, nnz) + 1e-3).astype(np.float32)
     return rp, col, val
+
+
+# ---------------------------------------------------------------- the same generator on the device
+# (graphgen_gpu.cu: c4 / c5 sizes, and one rank's rows without the whole edge list on the host)
+_GLIB = None
+
+
+def _glib():
+    global _GLIB
+    if _GLIB is None:
+        path = os.path.join(_HERE, "libgraphgen_gpu.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make` (or __graft_entry__.build())")
+        L = ctypes.CDLL(path)
+        u64p = ctypes.POINTER(ctypes.c_uint64)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.ggg_last_error.restype = ctypes.c_char_p
+        L.ggg_rmat.restype = ctypes.c_int
+        L.ggg_rmat.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                               ctypes.POINTER(u64p), ctypes.POINTER(ctypes.c_int64)]
+        L.ggg_free.argtypes = [ctypes.c_void_p]
+        L.ggg_free.restype = None
+        L.ggg_host_free.argtypes = [ctypes.c_void_p]
+        L.ggg_host_free.restype = None
+        L.ggg_to_host.restype = ctypes.c_int
+        L.ggg_to_host.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.ggg_degrees.restype = ctypes.c_int
+        L.ggg_degrees.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        L.ggg_owned_cols.restype = ctypes.c_int
+        L.ggg_owned_cols.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_int32, ctypes.POINTER(i32p), ctypes.POINTER(ctypes.c_int64)]
+        _GLIB = L
+    return _GLIB
+
+
+def _gcheck(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed rc={rc}: {_glib().ggg_last_error().decode()}")
+
+
+# iteration-matrix kinds of DeviceGraph.owned_rows
+KIND_A, KIND_AT, KIND_HITS = 0, 1, 2
+
+
+class DeviceGraph:
+    """The keys of make_graph(config) (R-MAT configs only), generated on `device` and kept there.
+    Bit-identical to the host generator.  Free with close() (the keys of c5 take 44 GB)."""
+
+    def __init__(self, config: str, device: int = 0, **override):
+        spec = dict(CONFIGS[config])
+        spec.update(override)
+        if spec.pop("kind") != "rmat":
+            raise ValueError("DeviceGraph: R-MAT configurations only")
+        self.name, self.n, self.device = config, int(spec["n"]), device
+        ptr = ctypes.POINTER(ctypes.c_uint64)()
+        mo = ctypes.c_int64(0)
+        _gcheck(_glib().ggg_rmat(spec["scale"], spec["n"], spec["m"], spec["a"], spec["b"], spec["c"],
+                                 spec.get("seed", SEED_GRAPH), spec.get("relabel_seed", SEED_RELABEL), device,
+                                 ctypes.byref(ptr), ctypes.byref(mo)), "ggg_rmat")
+        self._d = ctypes.cast(ptr, ctypes.c_void_p).value
+        self.m = int(mo.value)
+        self._deg = None
+
+    def close(self):
+        if self._d:
+            _glib().ggg_free(ctypes.c_void_p(self._d))
+            self._d = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def keys(self) -> np.ndarray:
+        out = np.empty(max(self.m, 1), dtype=np.uint64)
+        _gcheck(_glib().ggg_to_host(ctypes.c_void_p(self._d), self.m, out.ctypes.data), "ggg_to_host")
+        return out[: self.m]
+
+    def degrees(self):
+        """(out_degree, in_degree), int32 [n] each."""
+        if self._deg is None:
+            od = np.empty(self.n, dtype=np.int32)
+            idg = np.empty(self.n, dtype=np.int32)
+            _gcheck(_glib().ggg_degrees(ctypes.c_void_p(self._d), self.m, self.n, od.ctypes.data, idg.ctypes.data),
+                    "ggg_degrees")
+            self._deg = (od, idg)
+        return self._deg
+
+    def row_lengths(self, kind: int) -> np.ndarray:
+        """Row lengths of the iteration matrix (int64): A (out-degree), A^T (in-degree) or the HITS
+        block [[0, A^T], [A, 0]] (in-degrees then out-degrees)."""
+        od, idg = self.degrees()
+        if kind == KIND_A:
+            return od.astype(np.int64)
+        if kind == KIND_AT:
+            return idg.astype(np.int64)
+        return np.concatenate([idg, od]).astype(np.int64)
+
+    def owned_rows(self, kind: int, owner: np.ndarray, q: int):
+        """Rank q's rows of the iteration matrix: (owned_ids int32 ascending, row_ptr int64, col int32),
+        columns ascending within each row (global ids; HITS block: rows v < n hold n + u)."""
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        lens = self.row_lengths(kind)
+        if len(owner) != len(lens):
+            raise ValueError("owner must cover every row of the iteration matrix")
+        ids = np.nonzero(owner == q)[0]
+        rp = np.zeros(len(ids) + 1, dtype=np.int64)
+        np.cumsum(lens[ids], out=rp[1:])
+        ptr = ctypes.POINTER(ctypes.c_int32)()
+        cnt = ctypes.c_int64(0)
+        _gcheck(_glib().ggg_owned_cols(ctypes.c_void_p(self._d), self.m, self.n, kind, owner.ctypes.data, q,
+                                       ctypes.byref(ptr), ctypes.byref(cnt)), "ggg_owned_cols")
+        c = int(cnt.value)
+        if c != int(rp[-1]):
+            _glib().ggg_host_free(ctypes.cast(ptr, ctypes.c_void_p))
+            raise RuntimeError(f"owned_rows: {c} columns for row lengths summing to {int(rp[-1])}")
+        col = np.ctypeslib.as_array(ptr, shape=(max(c, 1),))[:c].copy()
+        _glib().ggg_host_free(ctypes.cast(ptr, ctypes.c_void_p))
+        return ids.astype(np.int32), rp, col

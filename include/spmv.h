@@ -254,12 +254,17 @@ spmv_status spmv_solver_create(int algo, int64_t n, int64_t m, const int64_t* ro
  * of [0, n_global) owned by exactly one rank) and passes their rows of the iteration matrix with
  * global column ids -- PageRank: the in-neighbours u of each owned v (edges u -> v, Eq. 6;
  * duplicates already merged) plus out_degree[r] of each owned vertex; RWR: the neighbours in
- * A u A^T (Eq. 9; reading R8), out_degree NULL (the row length is the degree).  Ownership
+ * A u A^T (Eq. 9; reading R8), out_degree NULL (the row length is the degree); HITS: rows
+ * of the block matrix [[0, A^T], [A, 0]] (Eq. 8), owned_ids in [0, 2 n_global) -- row
+ * v < n_global lists n_global + u for every edge u -> v, row n_global + u lists v -- and
+ * out_degree NULL (a block row's length is also its column's length).  Ownership
  * and degrees of all vertices are exchanged once over the communicator (O(n) per rank); the
  * iteration is the allgather path of spmv_solver_create with comm.  Results and runs as for
  * spmv_solver_create (spmv_solver_result writes all n_global values on every rank).
- * Errors: EINVAL (null pointer, HITS, PageRank without out_degree, overlapping / missing
- * ownership, exchange = 1), ERANGE (id outside [0, n_global)), ENCCL, ECUDA. */
+ * On the loopback transport the ranks' builds run one at a time (they share the host's memory).
+ * Errors: EINVAL (null pointer, PageRank without out_degree, HITS with out_degree, overlapping /
+ * missing ownership, exchange = 1), ERANGE (id outside [0, n_global), HITS [0, 2 n_global)),
+ * ENCCL, ECUDA. */
 spmv_status spmv_solver_create_local(int algo, int64_t n_global, int64_t n_local, const int32_t* owned_ids,
                                      const int64_t* row_ptr, const int32_t* col, const int32_t* out_degree,
                                      const spmv_iter_opts* it, const spmv_options* opt, spmv_comm comm,
@@ -270,6 +275,11 @@ spmv_status spmv_solver_run(spmv_solver s, int64_t query, void* stream, spmv_ite
  * HITS authority a [n] in out0 and hub h [n] in out1. */
 spmv_status spmv_solver_result(spmv_solver s, float* out0, float* out1);
 spmv_status spmv_solver_plan_stats(spmv_solver s, spmv_plan_stats_t* out);
+/* Change the stopping rule between runs (spmv_iter_opts tol, max_iter, fixed_iters; reading R2):
+ * the plan, the exchange layout and every other option stay, so one build serves runs to several
+ * iteration counts (preprocessing amortised, L98).  Errors: EINVAL (null, tol < 0, max_iter < 1,
+ * fixed_iters < 0). */
+spmv_status spmv_solver_set_stop(spmv_solver s, double tol, int32_t max_iter, int32_t fixed_iters);
 int32_t spmv_solver_launches_per_iter(spmv_solver s);
 void spmv_solver_destroy(spmv_solver s);
 

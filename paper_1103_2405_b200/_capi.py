@@ -93,6 +93,7 @@ SIGNATURES = {
     "spmv_solver_plan_stats": (c_i32, [c_vp, ctypes.POINTER(PlanStats)]),
     "spmv_solver_run_batch": (c_i32, [c_vp, c_vp, c_i32, c_vp, ctypes.POINTER(IterResult)]),
     "spmv_solver_result_batch": (c_i32, [c_vp, c_vp]),
+    "spmv_solver_set_stop": (c_i32, [c_vp, c_f64, c_i32, c_i32]),
     "spmv_solver_launches_per_iter": (c_i32, [c_vp]),
     "spmv_solver_destroy": (None, [c_vp]),
     "pagerank": (c_i32, [c_i64, c_i64, c_vp, c_vp, ctypes.POINTER(IterOpts), ctypes.POINTER(Options),

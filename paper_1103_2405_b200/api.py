@@ -289,6 +289,11 @@ class Solver:
         check(C.lib().spmv_solver_plan_stats(self._h, ctypes.byref(s)), "spmv_solver_plan_stats")
         return _stats_dict(s)
 
+    def set_stop(self, tol: float = 1e-6, max_iter: int = 1000, fixed_iters: int = 0):
+        """Change the stopping rule for the next runs (spmv_solver_set_stop); the plan stays."""
+        check(C.lib().spmv_solver_set_stop(self._h, float(tol), int(max_iter), int(fixed_iters)),
+              "spmv_solver_set_stop")
+
     @property
     def launches_per_iter(self) -> int:
         return int(C.lib().spmv_solver_launches_per_iter(self._h))

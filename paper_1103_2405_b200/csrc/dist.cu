@@ -84,6 +84,10 @@ struct Loopback {
     std::vector<const int64_t*> offs;       // published per-peer offsets (needed mode)
     std::vector<cudaEvent_t> ready, done;   // per rank: data ready / copies out of it finished
     std::vector<std::vector<char>> host;    // metadata allgather
+    // the ranks' solver builds run one at a time: they share one host, and a c5 slice build holds
+    // several GB of host vectors (per-rank processes on a real box build on their own hosts' cores
+    // in parallel; here the builder's OpenMP loops already use every core)
+    std::mutex build_mu;
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
         const long g = gen;
@@ -539,6 +543,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
     if (it) s->it = *it; else spmv_iter_opts_default(&s->it, algo);
     D->P = comm->world; D->rank = comm->rank;
     spmv_status st = SPMV_OK;
+    std::unique_lock<std::mutex> build_lock;       // loopback: one rank's build at a time
     try {
         std::vector<int64_t> mrp, len; std::vector<int32_t> mcol;
         std::vector<int32_t> owner;
@@ -547,6 +552,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         int64_t S = 0;
         const int64_t nv = n;
         if (!li) {
+            if (comm->lb) build_lock = std::unique_lock<std::mutex>(comm->lb->build_mu);
             std::vector<int64_t> arp; std::vector<int32_t> acol;
             clean_adjacency(n, row_ptr, col, arp, acol);
             n = build_iteration_matrix(algo, nv, arp, acol, mrp, mcol, len);   // n := vector length N
@@ -571,6 +577,12 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
                                               : (int32_t)(li->row_ptr[r + 1] - li->row_ptr[r]);
             }
             if ((st = allgather_host(comm, mine.data(), all.data(), 2 * std::max<int64_t>(mx, 1), 2 /*ncclInt32*/, 4))) throw st;
+            std::vector<int32_t>().swap(mine);
+            if (comm->lb) build_lock = std::unique_lock<std::mutex>(comm->lb->build_mu);
+            // HITS: the rows are those of the block matrix [[0, A^T], [A, 0]] (Eq. 8),
+            // 2|V| of them; a row's length is also its column's length (the block is structurally
+            // symmetric), so it orders the exchange slots like the full-input path's column lengths
+            if (algo == SPMV_ALGO_HITS) n = 2 * nv;
             owner.assign(n, -1);
             len.assign(n, 0);
             const int64_t w = 2 * std::max<int64_t>(mx, 1);
@@ -581,6 +593,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
                     owner[v] = q;
                     len[v] = all[q * w + mx + r];
                 }
+            std::vector<int32_t>().swap(all);
             for (int64_t v = 0; v < n; ++v)
                 if (owner[v] < 0) { set_error("a vertex is owned by no rank"); throw SPMV_EINVAL; }
             in_row.assign(n, -1);
@@ -760,6 +773,9 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         CKD(cudaMemcpy(s->d_inv_e, inv_e.data(), ne * sizeof(float), cudaMemcpyHostToDevice));
         CKD(cudaMalloc(&s->d_fpos, nl * sizeof(int32_t)));
         if (D->n_local) CKD(cudaMemcpy(s->d_fpos, s->fpos.data(), D->n_local * sizeof(int32_t), cudaMemcpyHostToDevice));
+        // per-vertex host tables the iteration does not read (c5: 2 GB each per rank)
+        std::vector<int64_t>().swap(D->gpos);
+        if (algo != SPMV_ALGO_RWR) std::vector<int64_t>().swap(D->lrow);
 #undef CKD
     } catch (spmv_status code) {
         st = code;

@@ -293,12 +293,16 @@ spmv_status spmv_solver_create_local(int algo, int64_t n_global, int64_t n_local
         (n_local > 0 && row_ptr[n_local] > 0 && !col)) {
         set_error("invalid argument"); return SPMV_EINVAL;
     }
-    if (algo != SPMV_ALGO_PAGERANK && algo != SPMV_ALGO_RWR) { set_error("local input: PageRank or RWR"); return SPMV_EINVAL; }
+    if (algo != SPMV_ALGO_PAGERANK && algo != SPMV_ALGO_RWR && algo != SPMV_ALGO_HITS) {
+        set_error("local input: unknown algorithm"); return SPMV_EINVAL;
+    }
     if (algo == SPMV_ALGO_PAGERANK && n_local > 0 && !out_degree) { set_error("PageRank needs out_degree"); return SPMV_EINVAL; }
+    if (algo == SPMV_ALGO_HITS && out_degree) { set_error("HITS: out_degree must be NULL"); return SPMV_EINVAL; }
+    const int64_t n_rows = algo == SPMV_ALGO_HITS ? 2 * n_global : n_global;   // HITS: block rows
     if (n_local > 0 && row_ptr[0] != 0) { set_error("row_ptr[0] != 0"); return SPMV_EINVAL; }
     for (int64_t i = 0; i < n_local; ++i) {
         if (row_ptr[i + 1] < row_ptr[i]) { set_error("row_ptr not monotone"); return SPMV_EINVAL; }
-        if (owned_ids[i] < 0 || owned_ids[i] >= n_global) { set_error("owned id out of range"); return SPMV_ERANGE; }
+        if (owned_ids[i] < 0 || owned_ids[i] >= n_rows) { set_error("owned id out of range"); return SPMV_ERANGE; }
         if (out_degree && out_degree[i] < 0) { set_error("negative degree"); return SPMV_EINVAL; }
     }
     if (device < 0) { set_error("solvers need a device"); return SPMV_EINVAL; }
@@ -404,6 +408,13 @@ __attribute__((visibility("default")))
 spmv_status spmv_solver_plan_stats(spmv_solver s, spmv_plan_stats_t* out) {
     if (!s || !s->plan) { set_error("null solver"); return SPMV_EINVAL; }
     return spmv_plan_stats(s->plan, out);
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_solver_set_stop(spmv_solver s, double tol, int32_t max_iter, int32_t fixed_iters) {
+    if (!s || !(tol >= 0.0) || max_iter < 1 || fixed_iters < 0) { set_error("invalid argument"); return SPMV_EINVAL; }
+    s->it.tol = tol; s->it.max_iter = max_iter; s->it.fixed_iters = fixed_iters;   // read per run (Ctrl)
+    return SPMV_OK;
 }
 
 __attribute__((visibility("default"))) int32_t spmv_solver_launches_per_iter(spmv_solver s) {

@@ -128,7 +128,11 @@ def test_local_input_errors(gpu):
     ids = np.arange(G.n, dtype=np.int32)
     with pytest.raises(SpmvError):                     # PageRank without degrees
         Solver.local("pagerank", G.n, ids, rp, col, device=0, comm=comm1())
-    with pytest.raises(SpmvError):                     # HITS is not a local-input algorithm
+    with pytest.raises(SpmvError):                     # HITS: block rows n..2n-1 owned by nobody
         Solver.local("hits", G.n, ids, rp, col, device=0, comm=comm1())
+    ids2 = np.arange(2 * G.n, dtype=np.int32)
+    rp2 = np.concatenate([rp, np.full(G.n, rp[-1])]).astype(np.int64)
+    with pytest.raises(SpmvError):                     # HITS takes no out_degree
+        Solver.local("hits", G.n, ids2, rp2, col, out_degree=np.ones(2 * G.n, np.int32), device=0, comm=comm1())
     with pytest.raises(SpmvError):                     # a vertex owned by nobody
         Solver.local("rwr", G.n, ids[:-1], rp[:-1], col[:rp[-2]], device=0, comm=comm1())

@@ -174,3 +174,73 @@ def test_local_input_loopback(algo, gpu):
     else:
         ref, _ = oracle.rwr(G.n, G.row_ptr, G.col, q, fixed_iters=info["iterations"])
     assert np.abs(v.astype(np.float64) - ref).sum() < 1e-6, info
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+def test_hits_local_input_loopback(norm, gpu):
+    """HITS local input (Eq. 8): each rank passes its rows of the block matrix
+    [[0, A^T], [A, 0]] (2|V| rows: row v lists n + u for u -> v, row n + u lists v), round-robin
+    ownership over the block rows; equal on every rank and to the oracle at equal k."""
+    from paper_1103_2405_b200 import Solver
+    G = graphgen.make_graph("t_small")
+    n = G.n
+    rows = [[] for _ in range(2 * n)]
+    for u in range(n):
+        for v in G.col[G.row_ptr[u]:G.row_ptr[u + 1]].tolist():
+            rows[v].append(n + u)
+            rows[n + u].append(v)
+    rows = [sorted(set(r)) for r in rows]
+    P = 3
+
+    def fn(r, comm):
+        own = np.arange(r, 2 * n, P, dtype=np.int32)
+        rp = np.concatenate([[0], np.cumsum([len(rows[v]) for v in own])]).astype(np.int64)
+        col = np.array([c for v in own for c in rows[v]], np.int32)
+        s = Solver.local("hits", n, own, rp, col, device=0, comm=comm, iter_kw=dict(hits_norm=norm))
+        info = s.run(0, stream=0)
+        v = s.result()
+        s.close()
+        return [(info, v)]
+
+    outs = run_ranks(P, fn)
+    check_same(outs)
+    info, (a, h) = outs[0][0]
+    ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=norm, fixed_iters=info["iterations"])
+    bar_a = 1e-6 * (1.0 if norm == 1 else np.abs(ra).sum())
+    bar_h = 1e-6 * (1.0 if norm == 1 else np.abs(rh).sum())
+    assert np.abs(a - ra).sum() < bar_a and np.abs(h - rh).sum() < bar_h, info
+
+
+@pytest.mark.parametrize("algo", ["pagerank", "hits"])
+def test_local_input_device_rows(algo, gpu):
+    """The c4 / c5 route at small size: the device generator's rows of the iteration matrix per rank
+    (graphgen.DeviceGraph.owned_rows) under the bitonic partition of the library, P = 4 loopback
+    ranks, against the oracle on the host generator's graph at equal k."""
+    from paper_1103_2405_b200 import Solver, bitonic_partition
+    G = graphgen.make_graph("t_mid")
+    dg = graphgen.DeviceGraph("t_mid", device=0)
+    kind = graphgen.KIND_HITS if algo == "hits" else graphgen.KIND_AT
+    P = 4
+    owner = bitonic_partition(dg.row_lengths(kind), P)
+    od, _ = dg.degrees()
+    parts = [dg.owned_rows(kind, owner, q) for q in range(P)]
+    dg.close()
+
+    def fn(r, comm):
+        ids, rp, col = parts[r]
+        s = Solver.local(algo, G.n, ids, rp, col, out_degree=od[ids] if algo == "pagerank" else None,
+                         device=0, comm=comm, iter_kw=dict(hits_norm=1) if algo == "hits" else None)
+        info = s.run(0, stream=0)
+        v = s.result()
+        s.close()
+        return [(info, v)]
+
+    outs = run_ranks(P, fn)
+    check_same(outs)
+    info, v = outs[0][0]
+    if algo == "pagerank":
+        ref, _ = oracle.pagerank(G.n, G.row_ptr, G.col, fixed_iters=info["iterations"])
+        assert np.abs(v.astype(np.float64) - ref).sum() < 1e-6, info
+    else:
+        ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=1, fixed_iters=info["iterations"])
+        assert np.abs(v[0] - ra).sum() < 1e-6 and np.abs(v[1] - rh).sum() < 1e-6, info
