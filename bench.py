@@ -9,6 +9,9 @@ inputs resident in HBM.  Metric: SpMV GFLOP/s (= 2 m / step time); HBM GB/s and 
 HITS / RWR iteration rates on the same graph are reported beside it.
 N > 1 (torchrun): every rank runs its own replica of the workload (independent problems, no
 data-path collective): weak scaling, value = total flops of all ranks / max-over-ranks time.
+At every N, key "c4_pagerank": BASELINE configs[3] (it-2004-shaped, 1.15 B edges) PageRank
+row-partitioned over all ranks (strong scaling; one allgather of the next x per iteration), each
+rank generating its own rows on its GPU; device time max over ranks, plus its end-to-end time.
 `--impl reference` times the fp64 CPU oracle (the only reference this paper-only tier has).
 """
 from __future__ import annotations
@@ -166,6 +169,81 @@ def reference_arm(args):
                              "sample": f"full c2 SpMV x {steps} (fp64 CSR, OpenMP over rows)"},
             "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def c4_pagerank_leg(args, pkg, local, rank, world):
+    import torch
+    import torch.distributed as dist
+    import graphgen
+    out = {}
+    t_g = time.time()
+    dg = graphgen.DeviceGraph("c4", device=local)
+    n, m = dg.n, dg.m
+    od, idg = dg.degrees()
+    owner = pkg.bitonic_partition(idg.astype(np.int64), world)
+    ids, rp, col = dg.owned_rows(graphgen.KIND_AT, owner, rank)
+    del owner
+    keys = dg.keys() if world == 1 else None
+    dg.close()
+    gen_s = time.time() - t_g
+
+    def mx(v):
+        if world == 1:
+            return v
+        tt = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    comm = pkg.Comm.from_torch(local) if world > 1 else pkg.Comm(0, 1, b"\0" * 128, local)
+    t_b = time.time()
+    s = pkg.Solver.local("pagerank", n, ids, rp, col, out_degree=od[ids], device=local, comm=comm)
+    build_s = mx(time.time() - t_b)
+    del rp, col
+    s.run()                                   # warm-up
+    info = s.run()
+    ms = mx(info["ms_total"])
+    # end to end through the API: the solve plus the result on the host (the one-time gather of
+    # every rank's rows and its D2H copy), host wall clock, max over ranks
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ie = s.run()
+    p = s.result()
+    e2e_ms = mx((time.perf_counter() - t0) * 1e3)
+    out["c4_pagerank"] = {
+        "workload": f"c4: it-2004-shaped Graph500 R-MAT s26, n={n}, m={m}, pattern",
+        "n_gpus": world, "scaling": "strong", "parallelism": f"row-partitioned x{world} (allgather)",
+        "iterations": info["iterations"], "iters_per_s": round(1e3 * info["iterations"] / ms, 1),
+        "ms_per_iter": round(ms / max(info["iterations"], 1), 3),
+        "phase_us": [round(mx(v), 1) for v in info["phase_us"]],
+        "predicted_us_per_iter_rank": round(info["predicted_us_per_iter"], 1),
+        "e2e": {"value": round(1e3 * ie["iterations"] / e2e_ms, 1), "unit": "iters/s",
+                "ms": round(e2e_ms, 2), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * n,
+                "note": "solve + result gather to host; the graph is resident (built once, L98)"},
+        "gen_s": round(mx(gen_s), 1), "build_s": round(build_s, 1),
+        "sum_p": round(float(np.sum(p, dtype=np.float64)), 6)}
+    s.close()
+    comm.close()
+    if world == 1:
+        # the single-GPU solver (no exchange, its own tile plan) on the same graph
+        G4 = graphgen.graph_from_keys("c4", n, keys)
+        del keys
+        t_b = time.time()
+        s4 = pkg.Solver("pagerank", G4.n, G4.row_ptr, G4.col, device=local)
+        b4 = time.time() - t_b
+        s4.run()
+        i4 = s4.run()
+        out["c4_pagerank_iters_per_s"] = round(1e3 * i4["iterations"] / i4["ms_total"], 1)
+        out["c4_pagerank_iterations"] = i4["iterations"]
+        out["c4_pagerank_us_per_iter"] = round(i4["us_per_iter"], 1)
+        out["c4_pagerank_predicted_us_per_iter"] = round(i4["predicted_us_per_iter"], 1)
+        out["c4_workload"] = f"it-2004-shaped Graph500 R-MAT s26, n={G4.n}, m={G4.m}, pattern, 1 GPU"
+        out["c4_gen_s"] = round(gen_s, 1)
+        out["c4_build_s"] = round(b4, 1)
+        s4.close()
+        del G4
+    return out
 
 
 def main():
@@ -414,27 +492,15 @@ def main():
         finally:
             gomp.omp_set_num_threads(len(os.sched_getaffinity(0)))
 
-    # BASELINE configs[3]: PageRank on the it-2004-shaped graph (41.3 M vertices, 1.15 B edges,
-    # x beyond L2) on this GPU; generation (~3 min) and the solver build are outside the timing
-    if rank == 0 and world == 1 and not args.no_extras and not args.no_c4:
+    # BASELINE configs[3]: PageRank on the it-2004-shaped graph (41.3 M vertices, 1.15 B edges, x
+    # beyond L2), row-partitioned over all N ranks (Sec. 3.2; strong scaling: one graph):
+    # every rank draws the graph on its own GPU (device generator, bit-identical to graphgen.c),
+    # keeps its rows of A^T under the library's bitonic partition and builds its local solver
+    # (spmv_solver_create_local); one allgather of the next x per iteration.  At N = 1 the same
+    # path runs with a world-1 communicator, and the single-GPU solver (no exchange) beside it.
+    if not args.no_extras and not args.no_c4:
         try:
-            t_g = time.time()
-            G4 = graphgen.make_graph("c4")
-            gen_s = time.time() - t_g
-            t_b = time.time()
-            s4 = pkg.Solver("pagerank", G4.n, G4.row_ptr, G4.col, device=local)
-            build_s = time.time() - t_b
-            s4.run()
-            i4 = s4.run()
-            extras["c4_pagerank_iters_per_s"] = round(1e3 * i4["iterations"] / i4["ms_total"], 1)
-            extras["c4_pagerank_iterations"] = i4["iterations"]
-            extras["c4_pagerank_us_per_iter"] = round(i4["us_per_iter"], 1)
-            extras["c4_pagerank_predicted_us_per_iter"] = round(i4["predicted_us_per_iter"], 1)
-            extras["c4_workload"] = f"it-2004-shaped Graph500 R-MAT s26, n={G4.n}, m={G4.m}, pattern, 1 GPU"
-            extras["c4_gen_s"] = round(gen_s, 1)
-            extras["c4_build_s"] = round(build_s, 1)
-            s4.close()
-            del G4
+            extras.update(c4_pagerank_leg(args, pkg, local, rank, world))
         except Exception as ex:
             extras["c4_error"] = str(ex)[:300]
 

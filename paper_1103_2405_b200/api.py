@@ -23,6 +23,29 @@ def _ptr(a):
     return None if a is None or a.size == 0 else a.ctypes.data
 
 
+def _need(cond, msg):
+    """argument validation that survives `python -O` (the C side trusts sizes it is given)"""
+    if not cond:
+        raise ValueError(msg)
+
+
+def _csr(n_rows, row_ptr, col, what="matrix"):
+    rp = _np(row_ptr, np.int64)
+    cl = _np(col, np.int32)
+    if int(n_rows) < 0:          # the library reports it (SPMV_EINVAL)
+        return rp, cl
+    _need(rp.ndim == 1 and len(rp) == int(n_rows) + 1, f"{what}: len(row_ptr) must be n_rows + 1 = {int(n_rows) + 1}")
+    _need(len(rp) == 0 or (rp[0] == 0 and int(rp[-1]) <= len(cl)), f"{what}: row_ptr[0] must be 0 and row_ptr[-1] <= len(col)")
+    return rp, cl
+
+
+def _dev_vec(t, n, name):
+    _need(hasattr(t, "data_ptr") and getattr(t, "is_cuda", False), f"{name} must be a CUDA tensor")
+    _need(str(t.dtype) == "torch.float32", f"{name} must be float32")
+    _need(t.is_contiguous(), f"{name} must be contiguous")
+    _need(t.numel() >= n, f"{name} has {t.numel()} elements, needs {n}")
+
+
 def make_options(**kw) -> C.Options:
     """spmv_options with defaults (spmv_options_default) overridden by keyword arguments.
     workload_sizes may be a list (num_tiles + 1 values)."""
@@ -85,9 +108,9 @@ class Plan:
 
     def __init__(self, n_rows, n_cols, row_ptr, col, val=None, device=0, **options):
         self.n_rows, self.n_cols = int(n_rows), int(n_cols)
-        rp = _np(row_ptr, np.int64)
-        cl = _np(col, np.int32)
+        rp, cl = _csr(self.n_rows, row_ptr, col, "Plan")
         vv = None if val is None else _np(val, np.float32)
+        _need(vv is None or len(vv) >= int(rp[-1]), "Plan: len(val) < nnz")
         if vv is None:
             options.setdefault("pattern", 1)
         self.nnz = int(rp[-1]) if len(rp) else 0
@@ -113,8 +136,8 @@ class Plan:
     # -- execution (device tensors) ------------------------------------------------------
     def execute(self, x, y, stream=None, permuted=False):
         """y = A x on device tensors (float32, contiguous); asynchronous on `stream`."""
-        assert x.dtype == y.dtype and str(x.dtype) == "torch.float32" and x.is_cuda and y.is_cuda
-        assert x.is_contiguous() and y.is_contiguous()
+        _dev_vec(x, self.n_cols, "x")
+        _dev_vec(y, self.n_rows, "y")
         fn = C.lib().spmv_execute_permuted if permuted else C.lib().spmv_execute
         check(fn(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                  _stream_handle(stream)), "spmv_execute")
@@ -123,6 +146,7 @@ class Plan:
     def execute_host(self, x: np.ndarray, stream=None) -> np.ndarray:
         """host x -> device -> host y (copies inside; synchronises)."""
         xh = _np(x, np.float32)
+        _need(xh.ndim == 1 and len(xh) >= self.n_cols, f"x needs {self.n_cols} elements")
         y = np.empty(max(self.n_rows, 1), dtype=np.float32)
         check(C.lib().spmv_execute_host(self._h, _ptr(xh) or ctypes.c_void_p(0), y.ctypes.data,
                                         _stream_handle(stream)), "spmv_execute_host")
@@ -134,13 +158,16 @@ class Plan:
         if Y is None:
             Y = np.empty((X.shape[0], self.n_rows), dtype=np.float32)
         count = int(X.shape[0])
-        assert tuple(Y.shape) == (count, self.n_rows) and tuple(X.shape) == (count, self.n_cols)
+        _need(tuple(Y.shape) == (count, self.n_rows) and tuple(X.shape) == (count, self.n_cols),
+              f"X must be [count, {self.n_cols}] and Y [count, {self.n_rows}]")
+        for t, nm in ((X, "X"), (Y, "Y")):
+            if hasattr(t, "data_ptr"):
+                _need(not t.is_cuda, f"{nm} must be a host (ideally pinned) tensor")
+                _need(str(t.dtype) == "torch.float32" and t.is_contiguous(), f"{nm} must be contiguous float32")
+            else:
+                _need(t.flags.c_contiguous and t.dtype == np.float32, f"{nm} must be contiguous float32")
         xp = X.data_ptr() if hasattr(X, "data_ptr") else X.ctypes.data
         yp = Y.data_ptr() if hasattr(Y, "data_ptr") else Y.ctypes.data
-        if hasattr(X, "is_contiguous"):
-            assert X.is_contiguous() and Y.is_contiguous()
-        else:
-            assert X.flags.c_contiguous and Y.flags.c_contiguous and X.dtype == np.float32 and Y.dtype == np.float32
         check(C.lib().spmv_execute_host_batch(self._h, ctypes.c_void_p(xp), ctypes.c_void_p(yp), count,
                                               _stream_handle(stream)), "spmv_execute_host_batch")
         return Y
@@ -217,8 +244,7 @@ class Solver:
     def __init__(self, algo: str, n, row_ptr, col, device=0, comm=None, iter_kw=None, **options):
         self.algo, self.n = algo, int(n)
         self._comm = comm                      # the communicator must outlive the solver
-        rp = _np(row_ptr, np.int64)
-        cl = _np(col, np.int32)
+        rp, cl = _csr(self.n, row_ptr, col, "Solver")
         self.m = int(rp[-1])
         self._it = iter_opts(algo, **(iter_kw or {}))
         self._opt = make_options(**options)
@@ -237,9 +263,9 @@ class Solver:
         self.algo, self.n = algo, int(n_global)
         self._comm = comm
         ids = _np(owned_ids, np.int32)
-        rp = _np(row_ptr, np.int64)
-        cl = _np(col, np.int32)
+        rp, cl = _csr(len(ids), row_ptr, col, "Solver.local")
         deg = _np(out_degree, np.int32) if out_degree is not None else None
+        _need(deg is None or len(deg) == len(ids), "Solver.local: len(out_degree) must equal len(owned_ids)")
         self.m = int(rp[-1]) if len(rp) else 0
         self._it = iter_opts(algo, **(iter_kw or {}))
         self._opt = make_options(**options)

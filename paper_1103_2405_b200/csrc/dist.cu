@@ -109,6 +109,20 @@ static spmv_status nccl_status(int r, const char* what) {
     return SPMV_ENCCL;
 }
 
+// ids [0, n) ordered by (length desc, id asc): a stable counting sort over the lengths (O(n + max
+// length); the c5 block has 267 M rows, where a comparison sort costs a minute per call)
+template <class Len>
+static std::vector<int64_t> order_by_length_desc(int64_t n, Len len) {
+    int64_t mx = 0;
+    for (int64_t i = 0; i < n; ++i) mx = std::max<int64_t>(mx, len(i));
+    std::vector<int64_t> start(mx + 2, 0);
+    for (int64_t i = 0; i < n; ++i) start[mx - len(i) + 1]++;        // bucket b = mx - length
+    for (int64_t b = 0; b <= mx; ++b) start[b + 1] += start[b];
+    std::vector<int64_t> order(n);
+    for (int64_t i = 0; i < n; ++i) order[start[mx - len(i)]++] = i;
+    return order;
+}
+
 extern "C" {
 
 __attribute__((visibility("default")))
@@ -117,9 +131,9 @@ spmv_status bitonic_partition(int64_t n_rows, const int64_t* row_len, int32_t P,
     if (P > std::max<int64_t>(n_rows, 1)) { set_error("P > rows"); return SPMV_ERANGE; }
     // rows by (length desc, id asc); sorted position s -> s mod P on even rounds, P-1-(s mod P)
     // on odd rounds (the previous round's longest-row recipient gets the shortest row, L108)
-    std::vector<int64_t> order(n_rows);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return row_len[a] > row_len[b]; });
+    for (int64_t i = 0; i < n_rows; ++i)
+        if (row_len[i] < 0) { set_error("negative row length"); return SPMV_EINVAL; }
+    const std::vector<int64_t> order = order_by_length_desc(n_rows, [&](int64_t i) { return row_len[i]; });
     for (int64_t s = 0; s < n_rows; ++s) {
         int64_t g = s / P, j = s % P;
         owner[order[s]] = (int32_t)((g % 2 == 0) ? j : P - 1 - j);
@@ -621,9 +635,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         // given in G positions, keep_col_order), so no per-iteration gather builds x from G.
         D->lrow.resize(n);
         {
-            std::vector<int64_t> order(n);
-            std::iota(order.begin(), order.end(), 0);
-            std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return len[a] > len[b]; });
+            const std::vector<int64_t> order = order_by_length_desc(n, [&](int64_t i) { return len[i]; });
             std::vector<int64_t> next(D->P, 0);
             for (int64_t i : order) D->lrow[i] = next[owner[i]]++;
         }

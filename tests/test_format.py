@@ -320,3 +320,22 @@ def test_tile_coo_bit_exact(seed):
         zip(np.repeat(np.arange(nr), np.diff(rp)).tolist(), col.tolist(), exp_v.astype(np.float64).tolist()))
     r2, c2, v2 = p.to_coo()
     assert sorted(zip(r2.tolist(), c2.tolist())) == sorted(zip(r.tolist(), c.tolist()))
+
+
+def test_binding_rejects_bad_shapes():
+    """The binding checks sizes before any C call (ValueError, also under python -O)."""
+    from paper_1103_2405_b200 import Plan, Solver
+    rp = np.array([0, 2, 3]); col = np.array([0, 1, 1], np.int32)
+    with pytest.raises(ValueError):
+        Plan(3, 2, rp, col, None, device=-1)               # len(row_ptr) != n_rows + 1
+    with pytest.raises(ValueError):
+        Plan(2, 2, rp, col[:2], None, device=-1)           # row_ptr[-1] > len(col)
+    with pytest.raises(ValueError):
+        Plan(2, 2, rp, col, np.ones(2, np.float32), device=-1)   # len(val) < nnz
+    p = Plan(2, 2, rp, col, None, device=-1)
+    with pytest.raises(ValueError):
+        p.execute_host(np.ones(1, np.float32))             # x shorter than n_cols
+    with pytest.raises(ValueError):
+        p.execute_host_batch(np.ones((2, 3), np.float32))  # wrong X shape
+    with pytest.raises(ValueError):
+        Solver.local("rwr", 2, np.array([0, 1], np.int32), rp, col, out_degree=np.ones(3, np.int32))

@@ -243,9 +243,12 @@ def test_config3_c4_pagerank_full_size(gpu):
     """BASELINE configs[3] (it-2004-shaped, 41.3 M vertices, 1.15 B edges, x beyond L2) on one B200:
     PageRank to 1e-6 L1 (Eq. 6, reading R1), within 1e-6 L1 of the fp64 oracle at equal k, and the
     stop rule equal to the oracle's own (+-1, reading R14).  About 5 minutes (generation and the
-    oracle dominate)."""
+    oracle dominate).  The graph comes from the device generator (bit-identical to graphgen.c,
+    tests/test_gpu_graphgen.py), which takes seconds where the host generator takes minutes."""
     from paper_1103_2405_b200 import Solver
-    G = graphgen.make_graph("c4")
+    dg = graphgen.DeviceGraph("c4", device=0)
+    G = graphgen.graph_from_keys("c4", dg.n, dg.keys())
+    dg.close()
     s = Solver("pagerank", G.n, G.row_ptr, G.col, device=0)
     info = s.run()
     p = s.result().astype(np.float64)
