@@ -10,7 +10,7 @@ PKG       := paper_1103_2405_b200
 CSRC      := $(PKG)/csrc
 LIBDIR    := $(PKG)/lib
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
-             -Iinclude -I$(CSRC) --expt-relaxed-constexpr -Xptxas -v
+             -Iinclude -I$(CSRC) --expt-relaxed-constexpr -Xptxas -v -Xcompiler -fopenmp
 CXXFLAGS  := -O3 -std=c++17 -fPIC -fvisibility=hidden -fopenmp -Iinclude -I$(CSRC) -I/usr/local/cuda/include -Wall -Wno-unused-function
 
 CU_SRCS   := $(wildcard $(CSRC)/*.cu)

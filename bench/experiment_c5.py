@@ -33,15 +33,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c5")
-    ap.add_argument("--P", type=int, default=8)
-    ap.add_argument("--iters", type=int, default=12)
-    ap.add_argument("--out", default=None)
-    ap.add_argument("--no-parity", action="store_true")
-    args = ap.parse_args()
-
+def run(config="c5", P=8, iters=12, parity=True):
+    """The whole route; returns the record (parity under rec["parity"] when parity=True)."""
+    args = argparse.Namespace(config=config, P=P, iters=iters, no_parity=not parity)
     import graphgen
     import paper_1103_2405_b200 as pkg
 
@@ -112,8 +106,9 @@ def main():
         c.close()
     if err:
         raise err[0]
-    rec["build_s_max"] = round(max(build_s), 1)
-    rec["build_s_sum"] = round(sum(build_s), 1)
+    # the loopback builds run one at a time: the last rank's create call spans all of them
+    rec["build_s_all_ranks"] = round(max(build_s), 1)
+    rec["build_ms_per_rank_plan"] = None
     i2 = [o["last"][0] for o in out]
     ms = max(i["ms_total"] for i in i2)
     rec["iterations"] = i2[0]["iterations"]
@@ -124,6 +119,7 @@ def main():
     rec["phase_us_max"] = [round(max(i["phase_us"][k] for i in i2), 1) for k in range(3)]
     rec["predicted_us_per_iter_rank_max"] = round(max(i["predicted_us_per_iter"] for i in i2), 1)
     rec["plan"] = [o["stats"] for o in out]
+    rec["build_ms_per_rank_plan"] = [round(o["stats"]["build_ms"], 1) for o in out]
     # algorithmic bytes per iteration (HITS block, pattern): 4 B per entry + 12 B per row,
     # plus 20 B per row for the epilogue / normalisation
     alg = 4 * 2 * m + 12 * 2 * n + 20 * 2 * n
@@ -155,6 +151,18 @@ def main():
             zero_rows_exact=bool(np.all(a2[ra == 0] == 0) and np.all(h2[rh == 0] == 0)),
             ok=bool(da.sum() < 1e-6 and dh.sum() < 1e-6))
         print(f"[c5] parity {rec['parity']}", flush=True)
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--P", type=int, default=8)
+    ap.add_argument("--iters", type=int, default=12)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    rec = run(args.config, args.P, args.iters, not args.no_parity)
     line = json.dumps(rec)
     print(line, flush=True)
     if args.out:

@@ -646,6 +646,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         D->gpos.resize(n);
         D->gpos_full.resize(n);
         D->owned.assign(cnt_all[D->rank], 0);
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; ++i) {
             D->gpos[i] = col_ne[i] ? (int64_t)owner[i] * D->slot + D->lrow[i] : -1;
             D->gpos_full[i] = (int64_t)owner[i] * D->S_full + D->lrow[i];
@@ -701,16 +702,23 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         std::vector<int64_t> lrp(D->n_local + 1, 0);
         for (int64_t r = 0; r < D->n_local; ++r) lrp[r + 1] = lrp[r] + row_len(D->owned[r]);
         std::vector<int32_t> lcol(lrp[D->n_local]);
-        for (int64_t r = 0; r < D->n_local; ++r) {
-            const int64_t v = D->owned[r];
-            const int32_t* c = row_cols(v);
-            const int64_t L = row_len(v);
-            for (int64_t k = 0; k < L; ++k) {
-                if (c[k] < 0 || c[k] >= n) { set_error("column out of range"); throw SPMV_EINVAL; }
-                const int64_t gp = gcol(c[k]);
-                if (gp < 0) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
-                lcol[lrp[r] + k] = (int32_t)gp;
+        {
+            // one pass over this rank's entries (c5: 1.4 G per rank), threads over rows
+            int bad = 0;
+            #pragma omp parallel for schedule(dynamic, 4096) reduction(|:bad)
+            for (int64_t r = 0; r < D->n_local; ++r) {
+                const int64_t v = D->owned[r];
+                const int32_t* c = row_cols(v);
+                const int64_t L = row_len(v);
+                for (int64_t k = 0; k < L; ++k) {
+                    if (c[k] < 0 || c[k] >= n) { bad |= 1; break; }
+                    const int64_t gp = gcol(c[k]);
+                    if (gp < 0) { bad |= 2; break; }
+                    lcol[lrp[r] + k] = (int32_t)gp;
+                }
             }
+            if (bad & 1) { set_error("column out of range"); throw SPMV_EINVAL; }
+            if (bad & 2) { set_error("internal: referenced column not exchanged"); throw SPMV_EINVAL; }
         }
         spmv_options opt;
         if (opt_in) opt = *opt_in; else spmv_options_default(&opt);
