@@ -10,6 +10,11 @@
 
 #include "launch.cuh"
 #include "pb_launch.cuh"
+
+#ifndef TC_PDL
+#define TC_PDL 1          // experiment builds: -DTC_PDL=0 launches every tile plainly (bench/explore_pdl.py)
+#endif
+
 #include "trace.h"
 #include "tune.h"
 
@@ -28,6 +33,7 @@ __global__ void permute_x_kernel(const float* __restrict__ x, const int32_t* __r
                                  float* __restrict__ xp, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    asm volatile("griddepcontrol.launch_dependents;");   // tile 0 may launch (it waits for us)
     for (; i < n; i += stride) xp[i] = __ldg(x + __ldcs(perm + i));
 }
 
@@ -40,6 +46,7 @@ __global__ void scatter_x_kernel(const float* __restrict__ x, const int32_t* __r
     const float4* x4 = reinterpret_cast<const float4*>(x);
     const int4* i4 = reinterpret_cast<const int4*>(inv);
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(inv)) & 15) == 0;
+    asm volatile("griddepcontrol.launch_dependents;");   // tile 0 may launch (it waits for us)
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (vec) {
         for (; i < n4; i += stride) {
@@ -295,6 +302,13 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     p->n_split = (int64_t)p->L.split.size() / 3;
     p->n_chunks = p->L.n_chunks;
     predict_plan(*p, pred);
+    // programmatic dependent launch between the standalone launches when they are short enough for
+    // the ~5 us launch gap to matter (measured, profiles/r02_pdl.log: 8 tiles of 16K columns on c2
+    // -3 %, c3 youtube 4 tiles -10 %; two 48K tiles on c2 +2.6 %, c4's 1 ms launches +0.8 %)
+    {
+        const int32_t nl = spmv_plan_launches(p);
+        p->pdl = TC_PDL && nl > 1 && p->predicted_us / nl < 64.0;
+    }
     for (int32_t t = 0; t < p->num_tiles; ++t)
         p->tiles[t].staged = (opt.stage_x != 0) && (p->tiles[t].col_hi - p->tiles[t].col_lo) * 4 <= 227 * 1024 &&
                              (p->tiles[t].col_lo % 4 == 0);
@@ -435,7 +449,7 @@ spmv_status execute_permuted(spmv_plan_s* p, const float* xp, float* y, cudaStre
         if (e) return cuda_status(e, "x alignment copy");
         return cuda_status(launch_pb(*p, p->pb_grid, xp, EpiStore{y}, st), "two-phase launch");
     }
-    return cuda_status(launch_tiles(*p, p->grid_tile, xp, EpiStore{y}, st), "tile launch");
+    return cuda_status(launch_tiles(*p, p->grid_tile, xp, EpiStore{y}, st, p->pdl), "tile launch");
 }
 
 }  // namespace tc

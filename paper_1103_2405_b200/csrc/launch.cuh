@@ -11,10 +11,27 @@ namespace tc {
 void set_error(const std::string& msg);
 spmv_status cuda_status(cudaError_t e, const char* what);
 
-// Launch tile t of `p` (x given relabelled: xp[k] = x[perm[k]]).
+// Kernel launch, with programmatic stream serialization when `pdl` (the kernel's
+// griddepcontrol.wait then orders it after the previous launch on the stream).
+template <class... Args>
+cudaError_t launch_k(void (*k)(Args...), int grid, int block, size_t smem, cudaStream_t st, bool pdl,
+                     Args... args) {
+    if (!pdl) { k<<<grid, block, smem, st>>>(args...); return cudaGetLastError(); }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid); cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem; cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// Launch tile t of `p` (x given relabelled: xp[k] = x[perm[k]]).  pdl: chained to the previous
+// launch on the stream by programmatic dependent launch (standalone products).
 template <class Epi>
 cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* xp,
-                        const Epi& epi, cudaStream_t st) {
+                        const Epi& epi, cudaStream_t st, bool pdl = false) {
     const TileInfo& ti = p.tiles[t];
     TileArgs a;
     a.desc = p.d_desc; a.wl_begin = ti.wl_begin; a.wl_end = ti.wl_end;
@@ -24,22 +41,20 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
     a.sched = p.d_sched + (kDynQ + 1) * t;
     if (ti.staged) {
         size_t smem = (size_t)a.width * sizeof(float);
-        if (p.pattern) tc_spmv_tile<true, false, Epi><<<grid, kThreads, smem, st>>>(a, epi);
-        else tc_spmv_tile<true, true, Epi><<<grid, kThreads, smem, st>>>(a, epi);
-    } else {
-        if (p.pattern) tc_spmv_tile<false, false, Epi><<<grid, kThreads, 0, st>>>(a, epi);
-        else tc_spmv_tile<false, true, Epi><<<grid, kThreads, 0, st>>>(a, epi);
+        if (p.pattern) return launch_k(tc_spmv_tile<true, false, Epi>, grid, kThreads, smem, st, pdl, a, epi);
+        return launch_k(tc_spmv_tile<true, true, Epi>, grid, kThreads, smem, st, pdl, a, epi);
     }
-    return cudaGetLastError();
+    if (p.pattern) return launch_k(tc_spmv_tile<false, false, Epi>, grid, kThreads, 0, st, pdl, a, epi);
+    return launch_k(tc_spmv_tile<false, true, Epi>, grid, kThreads, 0, st, pdl, a, epi);
 }
 
 // Launch every non-empty tile of `p` in ascending order.
 template <class Epi>
 cudaError_t launch_tiles(const spmv_plan_s& p, const std::vector<int>& grids, const float* xp,
-                         const Epi& epi, cudaStream_t st) {
+                         const Epi& epi, cudaStream_t st, bool pdl = false) {
     for (int32_t t = 0; t <= p.num_tiles; ++t) {
         if (p.tiles[t].wl_end == p.tiles[t].wl_begin) continue;
-        cudaError_t e = launch_tile(p, t, grids[t], xp, epi, st);
+        cudaError_t e = launch_tile(p, t, grids[t], xp, epi, st, pdl);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -47,6 +47,7 @@ struct spmv_plan_s {
     // two-phase tiles (pb.h): when set, the plan has no one-pass tiles; d_row_id holds the
     // two-phase row order (row | FLAG_FINAL, n_row_entries = n_rows) for the epilogues
     bool two_phase = false;
+    bool pdl = false;                   // standalone launches chained by programmatic dependent launch
     tc::PbLayout PB;                      // host copy; the per-entry arrays are released after upload
     bool pb_host_valid = false;
     int32_t* d_pb_runs = nullptr;

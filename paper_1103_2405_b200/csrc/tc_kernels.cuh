@@ -415,6 +415,11 @@ __device__ __forceinline__ void prefetch_workload(const TileArgs& a, int64_t j) 
 template <bool STAGED, bool VALUED, class Epi>
 __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(TileArgs a, Epi epi_in) {
     extern __shared__ float xs[];
+    // programmatic dependent launch (standalone multi-launch products, "restart a
+    // kernel for each tile"): the grid was launched while the previous launch (x relabel or tile)
+    // finished its last workloads; wait for it to complete and flush.  A no-op for launches
+    // without the PDL attribute (the solvers' graphs, single-launch plans).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     Epi epi = epi_in;
     if (!epi.begin()) return;                         // iteration loop already converged
     if (STAGED) {
@@ -505,6 +510,9 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
         run_workload<VALUED, false>(a, d, a.col + d.off, VALUED ? a.val + d.off : nullptr, x, epi, lane);
     }
 #endif
+    // this CTA's workloads are done: the next launch may start (triggering at kernel start instead
+    // measured slower on c2 multi-tile plans: profiles/r02_pdl.log)
+    asm volatile("griddepcontrol.launch_dependents;");
     epi.end();
 }
 
