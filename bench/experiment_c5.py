@@ -7,14 +7,16 @@ Route (nothing of size m ever exists whole on the host):
   1. the device generator draws the keys (graphgen.DeviceGraph, bit-identical to graphgen.c);
   2. the library's bitonic partition of the block rows by length (Sec. 3.2, L108) into P slices;
   3. each slice's rows of the block come off the device (DeviceGraph.owned_rows) -> host CSR;
-  4. P loopback ranks on this one GPU (spmv_comm_create_loopback) each build their row-partitioned
-     HITS solver from their slice (spmv_solver_create_local), one build at a time;
+  4. P ranks on this one GPU each build their row-partitioned HITS solver from their slice
+     (spmv_solver_create_local), one build at a time; by default they are slices of one solver
+     sharing one exchange buffer (spmv_comm_create_slices: the exchange is ordering only), or
+     (--transport loopback) each has its own buffer and pulls its peers' slots by device copies;
   5. K-1 and then K iterations at fixed k (spmv_solver_set_stop), device time max over ranks;
   6. parity: the oracle's fp64 product of the block with the GPU's iterate k-1, halves normalised
      (the paper's sum-1 rule, L440), against the GPU's iterate k -- every row.
-On one GPU the P ranks share the device, so the loopback exchange (device copies) and each rank's
-normalisation pass over the whole exchange buffer run P times in series: the per-phase split says
-how much of an iteration that is.
+With the loopback transport the P ranks' exchanges (device copies) and normalisation passes over
+their whole buffers run P times on the one device: the per-phase split says how much of an
+iteration that is; the slices transport does neither.
 
 python bench/experiment_c5.py [--config c5] [--P 8] [--iters 12] [--out file.jsonl]
 """
@@ -33,13 +35,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run(config="c5", P=8, iters=12, parity=True):
-    """The whole route; returns the record (parity under rec["parity"] when parity=True)."""
+def run(config="c5", P=8, iters=12, parity=True, transport="slices"):
+    """The whole route; returns the record (parity under rec["parity"] when parity=True).
+    transport "slices": the P ranks share one exchange buffer (spmv_comm_create_slices, no copies);
+    "loopback": each rank has its own buffer and pulls its peers' slots (the multi-GPU protocol)."""
     args = argparse.Namespace(config=config, P=P, iters=iters, no_parity=not parity)
     import graphgen
     import paper_1103_2405_b200 as pkg
 
-    rec = dict(config=args.config, P=args.P, iters=args.iters)
+    rec = dict(config=args.config, P=args.P, iters=args.iters, transport=transport)
     t = time.time()
     dg = graphgen.DeviceGraph(args.config, device=0)
     rec["gen_s"] = round(time.time() - t, 1)
@@ -59,7 +63,7 @@ def run(config="c5", P=8, iters=12, parity=True):
     del owner, lens
     print(f"[c5] partitioned + sliced in {rec['partition_s']} + {rec['slices_s']} s", flush=True)
 
-    comms = pkg.Comm.loopback(args.P, 0)
+    comms = pkg.Comm.slices(args.P, 0) if transport == "slices" else pkg.Comm.loopback(args.P, 0)
     out = [None] * args.P
     err = []
     build_s = [0.0] * args.P
@@ -161,8 +165,9 @@ def main():
     ap.add_argument("--iters", type=int, default=12)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--transport", default="slices", choices=["slices", "loopback"])
     args = ap.parse_args()
-    rec = run(args.config, args.P, args.iters, not args.no_parity)
+    rec = run(args.config, args.P, args.iters, not args.no_parity, args.transport)
     line = json.dumps(rec)
     print(line, flush=True)
     if args.out:

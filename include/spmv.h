@@ -342,6 +342,14 @@ spmv_status spmv_comm_create(int rank, int world, const void* nccl_unique_id, in
  * events and host barriers.  Lets the row-partitioned code path (slots, offsets, packing, rank-
  * order partial sums) run and be checked on one GPU.  Destroy every handle.  Errors: EINVAL, ECUDA. */
 spmv_status spmv_comm_create_loopback(int world, int device, spmv_comm* out);
+/* Row slices of one solver on one device (for matrices whose plan cannot be built in one piece on
+ * the host, e.g. BASELINE configs[4]'s 11 G-entry HITS block): as spmv_comm_create_loopback, but
+ * the ranks' solvers share one double-buffered exchange buffer (allocated by rank 0's solver at
+ * its first run): each rank writes its own slot, and the per-iteration exchange is only the
+ * ordering -- every rank's stream waits for every other rank's slot -- with no copies.  Same
+ * results as the loopback transport, bit for bit.  spmv_iter_opts.exchange must be 0.
+ * Errors: EINVAL, ECUDA; at the first run ENOMEM if the shared buffer cannot be allocated. */
+spmv_status spmv_comm_create_slices(int world, int device, spmv_comm* out);
 void spmv_comm_destroy(spmv_comm comm);
 
 const char* spmv_last_error(void);

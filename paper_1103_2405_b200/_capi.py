@@ -107,6 +107,7 @@ SIGNATURES = {
     "spmv_comm_unique_id": (c_i32, [c_vp]),
     "spmv_comm_create": (c_i32, [ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, ctypes.POINTER(c_vp)]),
     "spmv_comm_create_loopback": (c_i32, [ctypes.c_int, ctypes.c_int, c_vp]),
+    "spmv_comm_create_slices": (c_i32, [ctypes.c_int, ctypes.c_int, c_vp]),
     "spmv_comm_destroy": (None, [c_vp]),
     "spmv_last_error": (ctypes.c_char_p, []),
     "spmv_version": (ctypes.c_char_p, []),

@@ -432,6 +432,14 @@ class Comm:
         check(C.lib().spmv_comm_create_loopback(world, device, arr), "spmv_comm_create_loopback")
         return [cls(r, world, b"", device, _handle=ctypes.c_void_p(arr[r])) for r in range(world)]
 
+    @classmethod
+    def slices(cls, world: int, device: int = 0):
+        """`world` row slices of one solver on one device sharing one exchange buffer
+        (spmv_comm_create_slices); drive each returned communicator from its own thread."""
+        arr = (ctypes.c_void_p * world)()
+        check(C.lib().spmv_comm_create_slices(world, device, arr), "spmv_comm_create_slices")
+        return [cls(r, world, b"", device, _handle=ctypes.c_void_p(arr[r])) for r in range(world)]
+
     def close(self):
         if getattr(self, "_h", None):
             C.lib().spmv_comm_destroy(self._h)

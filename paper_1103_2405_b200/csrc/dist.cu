@@ -88,6 +88,13 @@ struct Loopback {
     // several GB of host vectors (per-rank processes on a real box build on their own hosts' cores
     // in parallel; here the builder's OpenMP loops already use every core)
     std::mutex build_mu;
+    // slices mode (spmv_comm_create_slices): the ranks are row slices of one solver on one device
+    // and share one double-buffered exchange buffer -- each writes its own slot, and the exchange
+    // is only the ordering (every rank waits for every other rank's slot), no copies
+    bool shared = false;
+    int device = 0;
+    float* sG[2] = {nullptr, nullptr};      // mailbox: rank 0's solver posts its buffers at its first run
+    int64_t sG_floats = -1;
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
         const long g = gen;
@@ -248,13 +255,14 @@ spmv_status spmv_comm_create(int rank, int world, const void* uid, int device, s
     return SPMV_OK;
 }
 
-__attribute__((visibility("default")))
-spmv_status spmv_comm_create_loopback(int world, int device, spmv_comm* out) {
+static spmv_status create_loopback(int world, int device, bool shared, spmv_comm* out) {
     if (!out || world < 1) { set_error("invalid argument"); return SPMV_EINVAL; }
     cudaError_t e = cudaSetDevice(device);
     if (e) return cuda_status(e, "cudaSetDevice");
     auto lb = std::make_shared<Loopback>();
     lb->world = world;
+    lb->shared = shared;
+    lb->device = device;
     lb->ptr.assign(world, nullptr);
     lb->offs.assign(world, nullptr);
     lb->ready.assign(world, nullptr);
@@ -274,6 +282,16 @@ spmv_status spmv_comm_create_loopback(int world, int device, spmv_comm* out) {
         out[r] = c;
     }
     return SPMV_OK;
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_comm_create_loopback(int world, int device, spmv_comm* out) {
+    return create_loopback(world, device, false, out);
+}
+
+__attribute__((visibility("default")))
+spmv_status spmv_comm_create_slices(int world, int device, spmv_comm* out) {
+    return create_loopback(world, device, true, out);
 }
 
 __attribute__((visibility("default"))) void spmv_comm_destroy(spmv_comm c) {
@@ -315,6 +333,8 @@ struct Dist {
     float* d_S = nullptr;                    // send buffer
     int32_t* d_sidx = nullptr;               // send position -> own slot position (-1: padding)
     int64_t n_send = 0;
+    bool shared = false;                     // slices mode: d_Gb shared by every rank's solver
+    bool owns_shared = false;                //   allocated (and freed) by rank 0's solver
 };
 
 // send buffer: S[i] = own slot[sidx[i]] (values of the vertices a peer reads, then the partials)
@@ -493,10 +513,24 @@ spmv_status allgather(spmv_comm c, float* G, int64_t slot, cudaStream_t st) {
                        "ncclAllGather");
 }
 
+// slices mode: every rank's stream waits for every other rank's work enqueued so far (its slot of
+// the shared buffer written); two host barriers around the waits, as in loopback_pull
+spmv_status sync_ranks(spmv_comm c, cudaStream_t st) {
+    Loopback& L = *c->lb;
+    const int r = c->rank;
+    cudaError_t e = cudaEventRecord(L.ready[r], st);
+    L.barrier();
+    for (int q = 0; q < c->world && !e; ++q)
+        if (q != r) e = cudaStreamWaitEvent(st, L.ready[q], 0);
+    L.barrier();                                        // events free for the next round
+    return cuda_status(e, "slices sync");
+}
+
 // the per-iteration exchange: one in-place allgather of equal slots, or (needed mode) the packed
-// per-peer segments by grouped point-to-point sends / receives
+// per-peer segments by grouped point-to-point sends / receives; slices mode: ordering only
 spmv_status exchange(spmv_comm c, Dist* D, float* G, const tc::Ctrl* ctrl, int sm_count, cudaStream_t st) {
     tc::Range r("exchange");
+    if (D->shared) return c->world == 1 ? SPMV_OK : sync_ranks(c, st);
     if (!D->exchange) return allgather(c, G, D->slot, st);
     if (c->world == 1) return SPMV_OK;
     if (D->n_send) dist_pack<<<sm_count * 2, 256, 0, st>>>(G, D->d_sidx, D->d_S, D->n_send, ctrl);
@@ -660,6 +694,8 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         int64_t g_floats = (int64_t)D->P * D->slot;
         D->exchange = s->it.exchange == 1;
         if (D->exchange && li) { set_error("exchange = 1 needs the full graph on every rank"); throw SPMV_EINVAL; }
+        D->shared = comm->lb && comm->lb->shared;
+        if (D->exchange && D->shared) { set_error("slices share one exchange buffer: exchange = 0 only"); throw SPMV_EINVAL; }
         std::vector<std::vector<int32_t>> recv;
         if (!D->exchange) {
             for (int32_t q = 0; q < D->P; ++q) part_off[q] = (int64_t)q * D->slot + D->S;
@@ -737,7 +773,7 @@ spmv_status solver_create_dist(int algo, int64_t n, int64_t m, const int64_t* ro
         }
         s->n_dangling = n_dangling;
 #define CKD(x) do { if ((e = (x)) != cudaSuccess) { st = cuda_status(e, #x); throw st; } } while (0)
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 2 && !D->shared; ++b) {     // slices: shared buffers, set up at the first run
             CKD(cudaMalloc(&D->d_Gb[b], (size_t)g_floats * sizeof(float)));
             CKD(cudaMemset(D->d_Gb[b], 0, (size_t)g_floats * sizeof(float)));
         }
@@ -822,6 +858,28 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     }
     const int rwr = s->algo == SPMV_ALGO_RWR;
     const int hitsa = s->algo == SPMV_ALGO_HITS;
+    if (D->shared && !D->d_Gb[0]) {
+        // slices mode, first run: rank 0 allocates the shared double buffer (owned by its solver)
+        // and posts it; every rank picks it up between two barriers
+        Loopback& L = *s->comm->lb;
+        if (D->rank == 0) {
+            float* b[2] = {nullptr, nullptr};
+            const size_t bytes = (size_t)D->g_floats * sizeof(float);
+            if (!cudaMalloc(&b[0], bytes) && !cudaMalloc(&b[1], bytes) && !cudaMemset(b[0], 0, bytes) &&
+                !cudaMemset(b[1], 0, bytes) && !cudaDeviceSynchronize()) {
+                L.sG[0] = b[0]; L.sG[1] = b[1]; L.sG_floats = D->g_floats;
+                D->owns_shared = true;
+            } else {
+                cudaFree(b[0]); cudaFree(b[1]);
+                L.sG[0] = L.sG[1] = nullptr; L.sG_floats = -1;
+            }
+        }
+        L.barrier();
+        const bool ok = L.sG[0] && L.sG_floats == D->g_floats;
+        if (ok) { D->d_Gb[0] = L.sG[0]; D->d_Gb[1] = L.sG[1]; }
+        L.barrier();                                   // the mailbox is free for the next solver
+        if (!ok) { set_error("slices: shared exchange buffer unavailable"); return SPMV_ENOMEM; }
+    }
     D->q_local = -1;
     if (rwr && D->lrow[query] < D->n_local && D->owned[D->lrow[query]] == (int32_t)query) D->q_local = D->lrow[query];
     Ctrl c{};
@@ -835,9 +893,13 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
     auto own = [&](int b) { return D->exchange ? D->d_Gb[b] : D->d_Gb[b] + (int64_t)D->rank * D->slot; };
     const int g = p->sm_count * 4;
     spmv_status ss = SPMV_OK;
+    // slices mode: a rank touches only its own slot of the shared buffer
+    const int64_t own_lo = D->shared ? (int64_t)D->rank * D->slot : 0;
+    const int64_t own_n = D->shared ? D->S : D->g_floats;
     if (hitsa) {   // a(0) = h(0) = 1/|V| (L440): own rows and every gathered column
         fill_f<<<g, 256, 0, st>>>(s->d_p, D->n_local, (float)(1.0 / n));
-        g_fill_values<<<g, 256, 0, st>>>(D->d_Gb[0], D->d_col_half, D->g_floats, (float)(1.0 / n));
+        g_fill_values<<<g, 256, 0, st>>>(D->d_Gb[0] + own_lo, D->d_col_half + own_lo, own_n, (float)(1.0 / n));
+        if (D->shared && (ss = exchange(s->comm, D, D->d_Gb[0], s->d_ctrl, p->sm_count, st))) return ss;
     } else {
         dist_init<<<g, 256, 0, st>>>(s->d_p, own(0), s->d_inv, D->n_local, rwr, D->q_local, (float)(1.0 / n));
         init_entries<<<g, 256, 0, st>>>(s->d_p_e, p->d_row_id, p->n_row_entries, rwr, (int32_t)D->q_local, (float)(1.0 / n));
@@ -894,7 +956,9 @@ spmv_status solver_run_dist(spmv_solver s, int64_t query, void* stream, spmv_ite
                 // partials of the buffer the next iteration writes its product into
                 hits_dist_post<<<g, 512, 0, st>>>(zslot, s->d_p, D->d_half_local, D->n_local, s->d_ctrl, s->d_slots,
                                                   reinterpret_cast<double*>(own(launched & 1) + D->S) + 2);
-                hits_dist_scale<<<g, 256, 0, st>>>(Gn, D->d_col_half, D->g_floats, s->d_ctrl);
+                hits_dist_scale<<<g, 256, 0, st>>>(Gn + own_lo, D->d_col_half + own_lo, own_n, s->d_ctrl);
+                // slices: the next SpMV reads every rank's normalised slot
+                if (D->shared && (ss = exchange(s->comm, D, Gn, s->d_ctrl, p->sm_count, st))) return ss;
                 mark_iter();
                 ++launched;
                 continue;
@@ -992,7 +1056,8 @@ void solver_destroy_dist(spmv_solver s) {
     Dist* D = static_cast<Dist*>(s->dist);
     cudaSetDevice(s->device);
     if (D) {
-        cudaFree(D->d_Gb[0]); cudaFree(D->d_Gb[1]); cudaFree(D->d_half_local); cudaFree(D->d_col_half);
+        if (!D->shared || D->owns_shared) { cudaFree(D->d_Gb[0]); cudaFree(D->d_Gb[1]); }
+        cudaFree(D->d_half_local); cudaFree(D->d_col_half);
         cudaFree(D->d_part_off); cudaFree(D->d_S); cudaFree(D->d_sidx);
         delete D;
     }

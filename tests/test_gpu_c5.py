@@ -29,9 +29,10 @@ def _check(rec, config):
     assert p["max_rel_a"] < 1e-5 and p["max_rel_h"] < 1e-5, p
 
 
-def test_c5_route_s22(gpu):
+@pytest.mark.parametrize("transport", ["slices", "loopback"])
+def test_c5_route_s22(transport, gpu):
     import experiment_c5
-    _check(experiment_c5.run("c5_s22", P=8, iters=6), "c5_s22")
+    _check(experiment_c5.run("c5_s22", P=8, iters=6, transport=transport), "c5_s22")
 
 
 @pytest.mark.slow

@@ -17,10 +17,10 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def run_ranks(P, fn):
+def run_ranks(P, fn, transport="loopback"):
     """fn(rank, comm) in P threads; returns the per-rank results (re-raises the first error)."""
     from paper_1103_2405_b200 import Comm
-    comms = Comm.loopback(P, 0)
+    comms = Comm.slices(P, 0) if transport == "slices" else Comm.loopback(P, 0)
     out, err = [None] * P, []
 
     def body(r):
@@ -42,7 +42,7 @@ def run_ranks(P, fn):
     return out
 
 
-def solve(algo, G, P, exchange, q=0, norm=1, reps=2):
+def solve(algo, G, P, exchange, q=0, norm=1, reps=2, transport="loopback"):
     from paper_1103_2405_b200 import Solver
 
     def fn(r, comm):
@@ -57,7 +57,7 @@ def solve(algo, G, P, exchange, q=0, norm=1, reps=2):
         s.close()
         return res
 
-    return run_ranks(P, fn)
+    return run_ranks(P, fn, transport)
 
 
 def check_same(outs):
@@ -244,3 +244,27 @@ def test_local_input_device_rows(algo, gpu):
     else:
         ra, rh, _ = oracle.hits(G.n, G.row_ptr, G.col, norm=1, fixed_iters=info["iterations"])
         assert np.abs(v[0] - ra).sum() < 1e-6 and np.abs(v[1] - rh).sum() < 1e-6, info
+
+
+@pytest.mark.parametrize("algo,norm", [("pagerank", 1), ("rwr", 1), ("hits", 1), ("hits", 2)])
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_slices_equal_loopback(algo, norm, P, gpu):
+    """Slices mode (spmv_comm_create_slices: one shared exchange buffer, no copies) gives the
+    loopback transport's results bit for bit, on every rank, run to run."""
+    G = graphgen.make_graph("t_mid" if P == 3 else "t_small")
+    q = int(np.nonzero(np.diff(G.row_ptr) > 0)[0][1])
+    a = solve(algo, G, P, 0, q=q, norm=norm, transport="loopback")
+    b = solve(algo, G, P, 0, q=q, norm=norm, transport="slices")
+    check_same(b)
+    for x, y in zip(a[0], b[0]):
+        vx = x[1] if isinstance(x[1], tuple) else (x[1],)
+        vy = y[1] if isinstance(y[1], tuple) else (y[1],)
+        assert all(u.tobytes() == v.tobytes() for u, v in zip(vx, vy))
+        assert x[0]["iterations"] == y[0]["iterations"]
+
+
+def test_slices_reject_needed_exchange(gpu):
+    from paper_1103_2405_b200 import SpmvError
+    G = graphgen.make_graph("t_small")
+    with pytest.raises(SpmvError):
+        solve("pagerank", G, 2, 1, transport="slices")
