@@ -51,6 +51,7 @@ struct spmv_solver_s {
     std::vector<int32_t> fpos;      // host copy
     tc::Ctrl* d_ctrl = nullptr;
     double* d_slots = nullptr;
+    double pred_extra_us = 0.0;          // model terms beside the plan's SpMV (HITS normalisation)
     std::vector<int> grids;
     std::vector<int32_t> tiles_used, slot_base;
     int32_t total_slots = 0;

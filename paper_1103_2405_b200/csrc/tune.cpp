@@ -194,6 +194,11 @@ static const PerfTable& table_for(const char* path_opt) {
     return cache.emplace(path, T).first->second;
 }
 
+double stream_pass_us(const spmv_options& opt, double bytes) {
+    const PerfTable& T = table_for(opt.perf_table_path);
+    return T.launch_us + bytes / (T.stage_GBps * 1e3);
+}
+
 // ------------------------------------------------------------------ Alg. 3 on the packing walk
 // hist: (length, count) pairs, lengths descending (a tile's ranked rows).  Walks the same packing
 // rules as pack_layout and charges every workload to its wave.

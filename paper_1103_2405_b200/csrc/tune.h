@@ -18,5 +18,8 @@ PbParams pb_params(const spmv_options& opt, int64_t n_cols, int64_t nnz);
 double pb_predict_us(const spmv_options& opt, int64_t n_rows, int64_t n_cols, int64_t nnz, bool valued,
                      const PbParams& prm);
 double pb_predict_items_us(const spmv_options& opt, int64_t items, bool valued);
+// a streaming pass over `bytes` (one launch at the table's staging bandwidth): the HITS solvers'
+// normalisation pass beside the modelled SpMV (the paper's "two vector division", L440)
+double stream_pass_us(const spmv_options& opt, double bytes);
 
 }  // namespace tc
