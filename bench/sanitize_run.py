@@ -2,7 +2,8 @@
 (single tile, staged multi-tile, paper mode), two-phase SpMV, and the PageRank / HITS / RWR
 epilogue kernels through the row-partitioned solver at world 1 (a host-driven loop: the
 single-GPU solvers run inside a CUDA graph with a WHILE node, which the sanitizer tools do not
-instrument).  Usage: python bench/sanitize_run.py [c1|t_small]"""
+instrument), the slices transport at 3 ranks and batched RWR's host-driven loop.  The multi-tile
+one-pass plan is chained by programmatic dependent launch.  Usage: python bench/sanitize_run.py [c1|t_small]"""
 import os
 import sys
 
@@ -37,4 +38,29 @@ for algo in ("pagerank", "hits", "rwr"):
         print(cfg, algo, "exchange", ex, info["iterations"], flush=True)
         s.close()
 comm.close()
+# round 2: the slices transport (3 row slices of one solver sharing one exchange buffer, one host
+# thread each) and batched RWR through its host-driven loop
+import threading  # noqa: E402
+for algo in ("pagerank", "hits"):
+    comms = pkg.Comm.slices(3, 0)
+    outs = [None] * 3
+
+    def body(r):
+        s = pkg.Solver(algo, G.n, G.row_ptr, G.col, device=0, comm=comms[r], iter_kw=dict(fixed_iters=3))
+        outs[r] = s.run(0, stream=0)["iterations"]
+        s.result()
+        s.close()
+    th = [threading.Thread(target=body, args=(r,)) for r in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for c in comms:
+        c.close()
+    print(cfg, algo, "slices", outs, flush=True)
+s = pkg.Solver("rwr", G.n, G.row_ptr, G.col, device=0, iter_kw=dict(fixed_iters=3, host_loop=1))
+deg = np.diff(G.row_ptr) + np.bincount(G.col, minlength=G.n)
+qs = np.nonzero(deg > 0)[0][:25]
+print(cfg, "rwr batch", s.run_batch(qs)["iterations"], flush=True)
+s.close()
 print("done")
