@@ -85,7 +85,8 @@ typedef struct {
                                 the composite split (Solution 3, L88) */
     int32_t pb_region;       /* two-phase: products per row-bin region (0 = 8192; 32..65535) */
     int32_t pb_chunk;        /* two-phase: entries per column chunk (0 = 8192) */
-    int32_t pb_xcap;         /* two-phase: columns per chunk x segment (0 = 8192; <= 65536) */
+    int32_t pb_xcap;         /* two-phase: columns per chunk x segment (0 = 6144, or 4096 when
+                              * 6144 would not leave two CTAs per SM; <= 65536) */
     int64_t pb_group;        /* two-phase: products per group of bins kept L2-resident between the
                                 phases (0 = chosen from the L2 size) */
     int32_t keep_col_order;  /* 1: skip the column relabel (Solution 2) and keep the caller's

@@ -135,7 +135,8 @@ static std::vector<PbItem> pb_queue(const PbLayout& B) {
 static spmv_status create_two_phase(spmv_plan_s* p, const Prepared& P, const int64_t* row_ptr,
                                     const int32_t* col, const float* val, const PbParams& prm,
                                     std::chrono::steady_clock::time_point t0, bool built) {
-    if (!built && !pb_build(p->n_rows, p->n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, p->PB)) {
+    if (!built && !pb_build_fit(p->n_rows, p->n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm,
+                                p->opt.pb_xcap > 0, p->PB)) {
         delete p; return SPMV_EINVAL;
     }
     PbLayout& B = p->PB;
@@ -274,7 +275,8 @@ spmv_status create_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     bool built = false;
     if (opt.two_phase == -1 && !one_pass_forced && nnz > 0 && p->two_phase_us < 1.25 * p->one_pass_us) {
         // close enough to matter: build the layout and predict from its actual item count
-        if (pb_build(n_rows, n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, p->PB)) {
+        if (pb_build_fit(n_rows, n_cols, row_ptr, col, p->pattern ? nullptr : val, p->pattern, prm, opt.pb_xcap > 0,
+                         p->PB)) {
             built = true;
             p->two_phase_us = pb_predict_items_us(opt, (int64_t)p->PB.items.size(), !p->pattern);
             p->two_phase = p->two_phase_us < p->one_pass_us;

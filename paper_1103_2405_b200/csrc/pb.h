@@ -77,7 +77,9 @@ struct PbParams {
     int32_t rcap = 6144;        // products per bin region (shared memory of one reduce)
     int32_t pcap = 9216;        // positions per bin block (<= 65535)
     int32_t maxrows = 1024;     // rows per bin (row order and meta staged with the region)
-    int32_t xcap = 4096;        // columns per chunk x segment (shared memory of one expand)
+    int32_t xcap = 6144;        // columns per chunk x segment (shared memory of one expand); a
+                                // layout whose stages would not fit two CTAs per SM is rebuilt
+                                // with kPbXcapFallback (pb_build_fit)
     int32_t ccap = 4096;        // entries per chunk
     int32_t nrcap = 1024;       // runs per chunk (run table in shared memory)
     int32_t heavy = 32;         // composite threshold of the reduce: rows >= heavy are warp-per-row
@@ -107,6 +109,16 @@ struct PbLayout {
 // Returns false (with set_error) when a parameter cannot hold the matrix.
 bool pb_build(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int32_t* col, const float* val,
               bool pattern, const PbParams& prm, PbLayout& L);
+
+// Shared memory of one CTA's stages that still lets two CTAs share an SM (228 KB per SM, 1 KB
+// reserved per CTA, the kernel's static shared memory): the persistent kernel needs two CTAs per SM
+// to overlap its pipelines (one CTA per SM measured 1.47x slower on c2, profiles/r02_pb_xcap.log)
+constexpr int64_t kPbTwoCtaSmem = 112 * 1024;   // two stages (kPbStages) per CTA
+constexpr int32_t kPbXcapFallback = 4096;
+// pb_build, and when the default x segment cap makes the stages too large for two CTAs per SM and
+// the caller did not fix the cap, again with kPbXcapFallback
+bool pb_build_fit(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int32_t* col, const float* val,
+                  bool pattern, PbParams prm, bool xcap_fixed, PbLayout& L);
 
 // Bytes of one pipeline stage of the persistent CTA (pb_kernels.cuh): a 128-byte header plus the
 // largest item's staged streams (expand: column/run words, values, x segment, run table; reduce:

@@ -293,4 +293,13 @@ bool pb_build(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int32_t* 
     return true;
 }
 
+bool pb_build_fit(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int32_t* col, const float* val,
+                  bool pattern, PbParams prm, bool xcap_fixed, PbLayout& L) {
+    if (!pb_build(n_rows, n_cols, rp, col, val, pattern, prm, L)) return false;
+    if (xcap_fixed || prm.xcap <= kPbXcapFallback || 2 * L.stage_bytes <= kPbTwoCtaSmem) return true;
+    prm.xcap = kPbXcapFallback;
+    L = PbLayout();
+    return pb_build(n_rows, n_cols, rp, col, val, pattern, prm, L);
+}
+
 }  // namespace tc
