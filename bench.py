@@ -466,6 +466,12 @@ def main():
                 bi = s.run_batch(qs)
                 extras["rwr_batch25_us_per_iter"] = round(bi["us_per_iter"], 1)
                 extras["rwr_batch25_query_iters_per_s"] = round(25 * 1e6 / bi["us_per_iter"], 1)
+                # capacity: the SpMM's lanes are 32 queries wide, so a full batch costs the same pass
+                q32 = rng.choice(np.nonzero(deg > 0)[0], size=32, replace=False)
+                s.run_batch(q32)
+                b32 = s.run_batch(q32)
+                extras["rwr_batch32_us_per_iter"] = round(b32["us_per_iter"], 1)
+                extras["rwr_batch32_query_iters_per_s"] = round(32 * 1e6 / b32["us_per_iter"], 1)
             s.close()
         # cpu_baseline: the oracle as it stands on this box's host cores, bounded sample
         import oracle
