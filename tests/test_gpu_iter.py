@@ -258,3 +258,28 @@ def test_config3_c4_pagerank_full_size(gpu):
     assert abs(p.sum() - 1.0) < 1e-4
     _, own = oracle.pagerank(G.n, G.row_ptr, G.col)
     assert abs(own.iterations - info["iterations"]) <= 1
+
+
+def test_set_stop_reuses_the_plan(gpu):
+    """spmv_solver_set_stop: one build, runs to several iteration counts; each equals a fresh solver
+    built for that count, bit for bit; invalid rules are rejected."""
+    from paper_1103_2405_b200 import Solver, SpmvError
+    G = graphgen.make_graph("t_mid")
+    s = Solver("pagerank", G.n, G.row_ptr, G.col, device=0, iter_kw=dict(fixed_iters=3))
+    s.run()
+    p3 = s.result()
+    s.set_stop(fixed_iters=7)
+    assert s.run()["iterations"] == 7
+    p7 = s.result()
+    for k, p in ((3, p3), (7, p7)):
+        f = Solver("pagerank", G.n, G.row_ptr, G.col, device=0, iter_kw=dict(fixed_iters=k))
+        f.run()
+        assert f.result().tobytes() == p.tobytes()
+        f.close()
+    s.set_stop(tol=1e-6)                                   # back to the convergence rule
+    info = s.run()
+    assert info["converged"] and info["residual"] < 1e-6
+    for bad in (dict(tol=-1.0), dict(max_iter=0), dict(fixed_iters=-2)):
+        with pytest.raises(SpmvError):
+            s.set_stop(**bad)
+    s.close()
