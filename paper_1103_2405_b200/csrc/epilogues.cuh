@@ -96,6 +96,7 @@ struct EpiAffine {
         return true;
     }
     struct Pre { float acc, p_old, inv; };
+    static constexpr bool kEntryState = true;    // p, 1/deg in entry order: prefetch_rm
     __device__ __forceinline__ int32_t slot(uint32_t ent, int32_t e) const {
         return e >= 0 ? e : __ldg(fpos + (ent & ROW_MASK));
     }
@@ -105,6 +106,14 @@ struct EpiAffine {
         const uint32_t r = ent & ROW_MASK;
         if (ent & FLAG_ACC) q.acc = y[r];
         if (ent & FLAG_FINAL) { const int32_t s = slot(ent, e); q.p_old = p[s]; q.inv = __ldg(inv_deg + s); }
+        return q;
+    }
+    __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t has_acc) const {
+        Pre q{0.0f, 0.0f, 0.0f};
+        if (e >= 0) { q.p_old = p[e]; q.inv = __ldg(inv_deg + e); }   // entry order: no wait on ent
+        if (ent == PAD_ROW) return q;
+        if (has_acc && (ent & FLAG_ACC)) q.acc = y[ent & ROW_MASK];
+        if (e == -1 && (ent & FLAG_FINAL)) { const int32_t s = slot(ent, e); q.p_old = p[s]; q.inv = __ldg(inv_deg + s); }
         return q;
     }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
@@ -162,12 +171,21 @@ struct EpiHitsSpmv {
         return true;
     }
     struct Pre { float acc; int half; };
+    static constexpr bool kEntryState = true;    // half flag in entry order: prefetch_rm
     __device__ __forceinline__ Pre prefetch(uint32_t ent, int32_t e) const {
         Pre q{0.0f, 0};
         if (ent == PAD_ROW) return q;
         const uint32_t r = ent & ROW_MASK;
         if (ent & FLAG_ACC) q.acc = y[r];
         if (ent & FLAG_FINAL) q.half = __ldg(half + (e >= 0 ? e : __ldg(fpos + r)));
+        return q;
+    }
+    __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t has_acc) const {
+        Pre q{0.0f, 0};
+        if (e >= 0) q.half = __ldg(half + e);                           // entry order: no wait on ent
+        if (ent == PAD_ROW) return q;
+        if (has_acc && (ent & FLAG_ACC)) q.acc = y[ent & ROW_MASK];
+        if (e == -1 && (ent & FLAG_FINAL)) q.half = __ldg(half + __ldg(fpos + (ent & ROW_MASK)));
         return q;
     }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }

@@ -39,6 +39,7 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
     a.x = xp + ti.col_lo; a.width = (int32_t)(ti.col_hi - ti.col_lo);
     a.split = p.d_split; a.partials = p.d_partials; a.counters = p.d_counters;
     a.sched = p.d_sched + (kDynQ + 1) * t;
+    a.has_acc = t > 0;                     // the first tile's rows are all first touches
     if (ti.staged) {
         size_t smem = (size_t)a.width * sizeof(float);
         if (p.pattern) return launch_k(tc_spmv_tile<true, false, Epi>, grid, kThreads, smem, st, pdl, a, epi);

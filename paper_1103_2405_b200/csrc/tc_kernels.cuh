@@ -82,6 +82,7 @@ struct TileArgs {
     float* partials;          // [n_chunks]
     int32_t* counters;        // [n_split], zero between launches
     uint32_t* sched;          // [kDynQ + 1]: claim queues, CTAs done; zero between launches
+    int32_t has_acc;          // rows of this launch may carry FLAG_ACC (not the plan's first tile)
 };
 
 // Slot loads: SMEM = false streams from global memory with evict-first (ld.global.cs); SMEM = true
@@ -240,15 +241,24 @@ __device__ __forceinline__ void run_rm(const TileArgs& a, const WlDesc& d, const
             if (okk[j]) uu[j].load(wc + r * d.w, VALUED ? wv + r * d.w : nullptr, 4 * q);
             // a row's entry and its epilogue operands are fetched when the row starts, so their
             // latency overlaps the row's slot loads and gathers
-            ei[j] = d.row_base + r;
-            en[j] = (v < V && v % upl == 0 && sl == 0 && r < d.h) ? __ldg(a.row_id + ei[j]) : PAD_ROW;
+            // ei = -2 where no row starts: the entry-order epilogue state of a row is requested
+            // with its row entry, without waiting for it (prefetch_rm)
+            const bool starts = v < V && v % upl == 0 && sl == 0 && r < d.h;
+            if constexpr (Epi::kEntryState) ei[j] = starts ? d.row_base + r : -2;
+            else ei[j] = d.row_base + r;
+            en[j] = starts ? __ldg(a.row_id + d.row_base + r) : PAD_ROW;
         }
     };
     issue(0, u, ok, ent_s, eix_s);
     for (int v0 = 0; v0 < V; v0 += UB) {
         typename Epi::Pre pre_s[UB];
         #pragma unroll
-        for (int j = 0; j < UB; ++j) pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j], eix_s[j]);
+        for (int j = 0; j < UB; ++j) {
+            if constexpr (Epi::kEntryState)
+                pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch_rm(ent_s[j], eix_s[j], a.has_acc);
+            else
+                pre_s[j] = (d.kind == KIND_SPLIT) ? typename Epi::Pre{} : epi.prefetch(ent_s[j], eix_s[j]);
+        }
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int v = v0 + j;
@@ -300,7 +310,13 @@ __device__ __forceinline__ void run_cm(const TileArgs& a, const WlDesc& d, const
     for (int u0 = 0; u0 < total; u0 += UB) {
         typename Epi::Pre pre[UB];
         #pragma unroll
-        for (int j = 0; j < UB; ++j) pre[j] = epi.prefetch(ent[j], d.row_base + lane + 32 * ((u0 + j) / nk));
+        for (int j = 0; j < UB; ++j) {
+            if constexpr (Epi::kEntryState)
+                pre[j] = epi.prefetch_rm(ent[j], (u0 + j + 1) % nk == 0 && u0 + j < total
+                                                     ? d.row_base + lane + 32 * ((u0 + j) / nk) : -2, a.has_acc);
+            else
+                pre[j] = epi.prefetch(ent[j], d.row_base + lane + 32 * ((u0 + j) / nk));
+        }
         #pragma unroll
         for (int j = 0; j < UB; ++j) {
             const int uu = u0 + j;
@@ -519,6 +535,9 @@ __global__ void __launch_bounds__(kThreads, STAGED ? 1 : TC_MINB) tc_spmv_tile(T
 // Epilogue interface: prefetch(ent, e) loads what the row's write needs (the partial sum of
 // earlier tiles when FLAG_ACC, epilogue operands) early; commit(ent, e, v, pre) stores the row's
 // value or applies the fused epilogue; write(ent, e, v) = commit(ent, e, v, prefetch(ent, e)).
+// prefetch_rm(ent, e, has_acc) is the one-pass tiles' form: e >= 0 is a row entry index whose
+// entry-order state is loaded without consulting ent (its load may still be in flight), e = -1 a
+// split row (state through fpos), e = -2 nothing; ent is read only for FLAG_ACC when has_acc.
 // e is the index of the row entry in row_id[] (consecutive lanes -> consecutive entries, so
 // per-row epilogue state kept in entry order is read and written coalesced); -1 for split rows.
 // y = A x writer (no epilogue)
@@ -530,6 +549,7 @@ struct EpiStore {
     __device__ __forceinline__ Pre prefetch(uint32_t ent, int32_t) const {
         return Pre{(ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f};
     }
+    static constexpr bool kEntryState = false;   // no entry-order state: the one-pass tiles use prefetch
     __device__ __forceinline__ void commit(uint32_t ent, int32_t, float v, const Pre& pre) { y[ent & ROW_MASK] = v + pre.acc; }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
     // two-phase tiles: per-row state of entries [e0, e0 + n) into L2 ahead of the rows (none here)
