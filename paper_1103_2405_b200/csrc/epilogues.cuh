@@ -111,9 +111,11 @@ struct EpiAffine {
     __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t has_acc) const {
         Pre q{0.0f, 0.0f, 0.0f};
         if (e >= 0) { q.p_old = p[e]; q.inv = __ldg(inv_deg + e); }   // entry order: no wait on ent
-        if (ent == PAD_ROW) return q;
-        if (has_acc && (ent & FLAG_ACC)) q.acc = y[ent & ROW_MASK];
-        if (e == -1 && (ent & FLAG_FINAL)) { const int32_t s = slot(ent, e); q.p_old = p[s]; q.inv = __ldg(inv_deg + s); }
+        // ent (whose load may still be in flight) is looked at only where it decides a load
+        if ((has_acc || e == -1) && ent != PAD_ROW) {
+            if (has_acc && (ent & FLAG_ACC)) q.acc = y[ent & ROW_MASK];
+            if (e == -1 && (ent & FLAG_FINAL)) { const int32_t s = slot(ent, e); q.p_old = p[s]; q.inv = __ldg(inv_deg + s); }
+        }
         return q;
     }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
@@ -183,9 +185,10 @@ struct EpiHitsSpmv {
     __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t has_acc) const {
         Pre q{0.0f, 0};
         if (e >= 0) q.half = __ldg(half + e);                           // entry order: no wait on ent
-        if (ent == PAD_ROW) return q;
-        if (has_acc && (ent & FLAG_ACC)) q.acc = y[ent & ROW_MASK];
-        if (e == -1 && (ent & FLAG_FINAL)) q.half = __ldg(half + __ldg(fpos + (ent & ROW_MASK)));
+        if ((has_acc || e == -1) && ent != PAD_ROW) {
+            if (has_acc && (ent & FLAG_ACC)) q.acc = y[ent & ROW_MASK];
+            if (e == -1 && (ent & FLAG_FINAL)) q.half = __ldg(half + __ldg(fpos + (ent & ROW_MASK)));
+        }
         return q;
     }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
