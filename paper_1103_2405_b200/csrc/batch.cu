@@ -47,6 +47,7 @@ struct BatchArgs {
     double* res_out;                    // [32]
     int32_t slot_base, total_slots, is_last;
     cudaGraphConditionalHandle cond;
+    int64_t zero_row;                   // a row of Z that is always zero (row N: padding, never written)
 };
 
 // The SpMM writes the product Y = W_pattern Z only (first touch stores, later tiles add): its
@@ -63,9 +64,12 @@ struct BatchEpi {
     }
 };
 
+// the x row of tile column c; the padding sentinel reads the zero row, so the load is
+// unconditional (a select on the loaded value made the compiler retire each load before issuing
+// the next one into the same register: profiles/r02_batch_rwr_tuning.log, run97)
 __device__ __forceinline__ float xrow(const BatchArgs& a, int32_t c, int lane) {
-    if (c == a.width) return 0.0f;
-    return __ldg(a.Z + (a.col_lo + c) * kQP + lane);
+    const int64_t row = c != a.width ? a.col_lo + c : a.zero_row;
+    return __ldg(a.Z + row * kQP + lane);
 }
 
 #ifndef TC_BATCH_U
@@ -120,9 +124,8 @@ __global__ void __launch_bounds__(512, 2) spmm_rwr_tile(BatchArgs a) {
     const int64_t gw = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
     const int64_t G = (int64_t)gridDim.x * warps;
     BatchEpi epi{a, lane};
-    // this lane's query column of the tile's x rows (plain L2 caching: evict-last / evict-first
-    // hints on the hub / tail rows measured slower on c2, 5.5-6.6 vs 4.3 ms per iteration)
-    const float* zl = a.Z + a.col_lo * kQP + lane;
+    // x rows with plain L2 caching (evict-last / evict-first hints on the hub / tail rows measured
+    // slower on c2, 5.5-6.6 vs 4.3 ms per iteration)
     for (int64_t j = a.wl_begin + gw; j < a.wl_end; j += G) {
         const WlDesc d = load_desc(a.desc + j);
         const int32_t* wc = a.col + d.off;
@@ -140,10 +143,7 @@ __global__ void __launch_bounds__(512, 2) spmm_rwr_tile(BatchArgs a) {
                 if (base == 0) cn = (s0 + 32 + lane < total) ? __ldcs(wc + s0 + 32 + lane) : a.width;
                 float xv[kRowU];
                 #pragma unroll
-                for (int t = 0; t < kRowU; ++t) {
-                    const int32_t c = __shfl_sync(0xffffffffu, cl, base + t);
-                    xv[t] = c != a.width ? __ldg(zl + (int64_t)c * kQP) : 0.0f;
-                }
+                for (int t = 0; t < kRowU; ++t) xv[t] = xrow(a, __shfl_sync(0xffffffffu, cl, base + t), lane);
                 if (next_end - s0 > kRowU) {              // no row ends in this step (warp-uniform)
                     #pragma unroll
                     for (int t = 0; t < kRowU; ++t) acc += xv[t];
@@ -311,6 +311,7 @@ static BatchArgs batch_args(spmv_solver_s* s, BatchState* B, int32_t t, int pari
     a.split = p->d_split; a.partials = B->partials; a.counters = p->d_counters;
     a.Z = B->Z[parity]; a.Znext = B->Z[parity ^ 1]; a.R = B->R; a.Y = B->Y; a.inv = B->inv;
     a.q = B->q; a.c = (float)s->it.c; a.ctrl = s->d_ctrl; a.slots = B->slots; a.res_out = B->res;
+    a.zero_row = B->N;                  // Z rows N .. N+3: zeroed at allocation, never written
     a.slot_base = slot_base; a.total_slots = total_slots; a.is_last = is_last; a.cond = cond;
     return a;
 }
