@@ -76,6 +76,7 @@ __device__ __forceinline__ float xrow(const BatchArgs& a, int32_t c, int lane) {
 #define TC_BATCH_U 16
 #endif
 constexpr int kRowU = TC_BATCH_U;       // x-row loads in flight per warp step
+static_assert(32 % kRowU == 0, "a step must not straddle the 32 column ids a warp holds");
 
 // row rr of a column-major 32-row slab (k-interleaved by kvec): its w slots sit at
 // sb + (k / kvec) * 32 kvec + rr kvec + k % kvec; 32 ids per warp load, then as row_dot
