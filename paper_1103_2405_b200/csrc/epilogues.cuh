@@ -108,6 +108,11 @@ struct EpiAffine {
         if (ent & FLAG_FINAL) { const int32_t s = slot(ent, e); q.p_old = p[s]; q.inv = __ldg(inv_deg + s); }
         return q;
     }
+    __device__ __forceinline__ Pre prefetch_entry(int32_t e) const {
+        Pre q{0.0f, 0.0f, 0.0f};
+        if (e >= 0) { q.p_old = p[e]; q.inv = __ldg(inv_deg + e); }
+        return q;
+    }
     __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t has_acc) const {
         Pre q{0.0f, 0.0f, 0.0f};
         if (e >= 0) { q.p_old = p[e]; q.inv = __ldg(inv_deg + e); }   // entry order: no wait on ent
@@ -180,6 +185,11 @@ struct EpiHitsSpmv {
         const uint32_t r = ent & ROW_MASK;
         if (ent & FLAG_ACC) q.acc = y[r];
         if (ent & FLAG_FINAL) q.half = __ldg(half + (e >= 0 ? e : __ldg(fpos + r)));
+        return q;
+    }
+    __device__ __forceinline__ Pre prefetch_entry(int32_t e) const {
+        Pre q{0.0f, 0};
+        if (e >= 0) q.half = __ldg(half + e);
         return q;
     }
     __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t has_acc) const {

@@ -40,6 +40,16 @@ cudaError_t launch_tile(const spmv_plan_s& p, int32_t t, int grid, const float* 
     a.split = p.d_split; a.partials = p.d_partials; a.counters = p.d_counters;
     a.sched = p.d_sched + (kDynQ + 1) * t;
     a.has_acc = t > 0;                     // the first tile's rows are all first touches
+    if (!a.has_acc) {                      // first touches only: FirstTouch<Epi> (tc_kernels.cuh)
+        const FirstTouch<Epi> ft(epi);
+        if (ti.staged) {
+            size_t smem = (size_t)a.width * sizeof(float);
+            if (p.pattern) return launch_k(tc_spmv_tile<true, false, FirstTouch<Epi>>, grid, kThreads, smem, st, pdl, a, ft);
+            return launch_k(tc_spmv_tile<true, true, FirstTouch<Epi>>, grid, kThreads, smem, st, pdl, a, ft);
+        }
+        if (p.pattern) return launch_k(tc_spmv_tile<false, false, FirstTouch<Epi>>, grid, kThreads, 0, st, pdl, a, ft);
+        return launch_k(tc_spmv_tile<false, true, FirstTouch<Epi>>, grid, kThreads, 0, st, pdl, a, ft);
+    }
     if (ti.staged) {
         size_t smem = (size_t)a.width * sizeof(float);
         if (p.pattern) return launch_k(tc_spmv_tile<true, false, Epi>, grid, kThreads, smem, st, pdl, a, epi);
@@ -74,6 +84,12 @@ cudaError_t setup_grids(spmv_plan_s& p, std::vector<int>& grids) {
     if ((e = cudaFuncGetAttributes(&fa, kst))) return e;
     const int max_dyn = optin - (int)fa.sharedSizeBytes;
     if ((e = cudaFuncSetAttribute(kst, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
+    {   // the first-touch instantiations launched for first tiles (launch_tile)
+        auto fst = p.pattern ? tc_spmv_tile<true, false, FirstTouch<Epi>> : tc_spmv_tile<true, true, FirstTouch<Epi>>;
+        auto fgl = p.pattern ? tc_spmv_tile<false, false, FirstTouch<Epi>> : tc_spmv_tile<false, true, FirstTouch<Epi>>;
+        if ((e = cudaFuncSetAttribute(fst, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
+        if ((e = cudaFuncSetAttribute(fgl, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
+    }
     int nb = 0;
     if ((e = cudaFuncSetAttribute(kgl, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn))) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kgl, kThreads, 0))) return e;

@@ -549,11 +549,27 @@ struct EpiStore {
     __device__ __forceinline__ Pre prefetch(uint32_t ent, int32_t) const {
         return Pre{(ent != PAD_ROW && (ent & FLAG_ACC)) ? y[ent & ROW_MASK] : 0.0f};
     }
-    static constexpr bool kEntryState = false;   // no entry-order state: the one-pass tiles use prefetch
+    static constexpr bool kEntryState = true;    // one-pass tiles: prefetch_rm / prefetch_entry
+    __device__ __forceinline__ Pre prefetch_rm(uint32_t ent, int32_t e, int32_t) const { return prefetch(ent, e); }
+    __device__ __forceinline__ Pre prefetch_entry(int32_t) const { return Pre{0.0f}; }
     __device__ __forceinline__ void commit(uint32_t ent, int32_t, float v, const Pre& pre) { y[ent & ROW_MASK] = v + pre.acc; }
     __device__ __forceinline__ void write(uint32_t ent, int32_t e, float v) { commit(ent, e, v, prefetch(ent, e)); }
     // two-phase tiles: per-row state of entries [e0, e0 + n) into L2 ahead of the rows (none here)
     __device__ __forceinline__ void prefetch_rows(int64_t, int32_t, uint64_t) const {}
+};
+
+// A launch whose rows are all first touches (a plan's first tile): no accumulating rows, so the
+// epilogue's prefetch needs only the entry-order state and never looks at the row entry, whose
+// load may still be in flight (ncu source view: the FLAG_ACC test on it was the one-pass SpMV's
+// top stall).  Same arithmetic and stores as Epi.
+template <class Epi>
+struct FirstTouch : Epi {
+    static constexpr bool kEntryState = true;
+    FirstTouch() = default;
+    __host__ __device__ explicit FirstTouch(const Epi& e) : Epi(e) {}
+    __device__ __forceinline__ typename Epi::Pre prefetch_rm(uint32_t, int32_t e, int32_t) const {
+        return this->prefetch_entry(e);
+    }
 };
 
 }  // namespace tc
