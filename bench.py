@@ -422,6 +422,33 @@ def main():
 
     extras, cpu = {}, None
     if rank == 0 and world == 1 and not args.no_extras:
+        # the other execution of the same format on the same workload: the one-pass tiles (x relabel
+        # + tile launches); the model picks between the two by predicted time (DESIGN 7c)
+        po = pkg.Plan(G.n, G.n, G.row_ptr, G.col, val, device=local, two_phase=0)
+        for _ in range(10):
+            po.execute(xt, yt, stream=stream)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(200):
+            po.execute(xt, yt, stream=stream)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        per_o = np.zeros(po.launches, np.float64)
+        bo = np.zeros(po.launches, np.float32)
+        for _ in range(20):
+            pkg._capi.check(pkg.lib().spmv_execute_timed(po._h, ctypes.c_void_p(xt.data_ptr()),
+                                                          ctypes.c_void_p(yt.data_ptr()),
+                                                          ctypes.c_void_p(stream.cuda_stream), bo.ctypes.data,
+                                                          po.launches), "spmv_execute_timed")
+            per_o += bo
+        per_o /= 20
+        tile_us = float(per_o[1:].sum()) * 1e3
+        sto = po.stats()
+        extras["one_pass"] = {"us_per_step": round(h0.elapsed_time(h1) * 1e3 / 200, 2),
+                              "launch_us": [round(float(v) * 1e3, 2) for v in per_o],
+                              "tile_frac_of_peak": round((8 * G.m + 12 * G.n) / (tile_us * 1e-6) / 1e9 / roofline["peak"], 4),
+                              "predicted_us": round(sto["predicted_us"], 1), "wl": sto["wl"], "num_tiles": sto["num_tiles"]}
+        po.close()
         # BASELINE configs[0] (R-MAT s16, ~1 M entries; L2-resident: launch/latency-bound, so
         # reported in microseconds, not against the roofline): SpMV and PageRank to 1e-6
         import graphgen
