@@ -470,9 +470,10 @@ PbParams pb_params(const spmv_options& opt, int64_t n_cols, int64_t nnz) {
 
 // Model of the two-phase tiles.  Both phases run out of shared-memory stages filled by bulk
 // copies, so time is set by how many items the persistent CTAs get through: t = items * t_item /
-// CTAs + launch, with t_item measured on B200 (a CTA's two-stage pipeline at two CTAs per SM:
-// 3.2 us per item valued, 2.95 us pattern; c2 valued 29.7 K items in 325 us, pattern 304 us; c4:
-// 1.05 M items in 13.7 ms).
+// CTAs + launch, with t_item measured on B200 (a CTA's two-stage pipeline at two CTAs per SM;
+// defaults 3.2 / 2.95 us valued / pattern from round-2's first layout (c2 29.7 K items in 325 us);
+// the shipped table carries 3.32 / 3.15 us, refitted to the x segment cap of 6144: c2 28.6 K items
+// in 325 / 309 us).
 // The item count is estimated from the parameters: bins of ~rcap products, and chunks cut by
 // whichever of ccap entries, xcap columns or nrcap distinct bins binds first.
 double pb_predict_us(const spmv_options& opt, int64_t n_rows, int64_t n_cols, int64_t nnz, bool valued,
